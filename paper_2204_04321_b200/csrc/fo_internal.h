@@ -1,0 +1,124 @@
+// fo_internal.h -- private structures of libfo (host + device side).
+// Layout and numbering: DESIGN.md "Layout in HBM"; public contract: include/fo.h.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fo.h"
+
+namespace fo {
+
+// Per-column record, 48 bytes, gathered by the assembly kernels (one per
+// extruded column; the paper's "boundary data aligned to its map" lesson,
+// every field a wedge needs is in one contiguous record).
+struct alignas(16) ColRec {
+  double x, y;       // footprint position (m)
+  double base, H;    // bed-side base z = s - H, thickness
+  double beta;       // basal friction after the floating mask
+  int64_t cs_n;      // (CSR value offset of the column's first row) << 8 | list length n_c
+};
+
+// Per-triangle record, 24 bytes: local column ids and the 9 structural slots
+// slot[i][j] = position of column v[j] in the sorted coupling list of v[i].
+struct alignas(8) TriRec {
+  int32_t v[3];
+  uint8_t slot[9];
+  uint8_t pad[3];
+};
+
+// Column-patch work decomposition of the owner-computes kernel.
+struct PatchPlan {
+  int32_t n_patches = 0;
+  int32_t max_tris = 0;          // max triangles of any patch (block capacity)
+  int32_t max_cols = 0;
+  std::vector<int32_t> col_begin;  // [n_patches+1] owned-column range of patch p
+  std::vector<int32_t> tri_ptr;    // [n_patches+1] into tri_list
+  std::vector<int32_t> tri_list;   // local triangle ids touching the patch's columns
+  // per patch-column incidence: for owned column c of patch p, the list of
+  // (patch-local triangle index << 2 | local vertex index of c) entries
+  std::vector<int32_t> inc_ptr;    // [n_owned_cols+1] global (over all patches)
+  std::vector<int32_t> inc;        // packed entries
+};
+
+struct DevPatch {
+  int32_t* col_begin = nullptr;
+  int32_t* tri_ptr = nullptr;
+  int32_t* tri_list = nullptr;
+  int32_t* inc_ptr = nullptr;
+  int32_t* inc = nullptr;
+};
+
+}  // namespace fo
+
+struct fo_mesh_s {
+  int device = 0;
+  fo_params p{};
+  int32_t L = 0;
+  int64_t n_col = 0, nA = 0, nB = 0, nC = 0;  // local columns by class
+  int64_t n_tri = 0;                          // local triangles
+  int64_t n_node = 0, n_dof = 0, n_elem = 0, n_owned_dof = 0;
+  int64_t nnz = 0;
+  // host topology (kept for graph / halo construction)
+  std::vector<int64_t> glob;       // local column -> global column
+  std::vector<int64_t> tri_glob;   // local triangle -> global triangle
+  std::vector<int32_t> tri;        // local triangles, local column ids
+  std::vector<int64_t> nbr_ptr;    // coupling lists (incl. self), sorted by local id
+  std::vector<int32_t> nbr;
+  std::vector<int64_t> colstart;   // [n_col+1] CSR value offset of each column block
+  std::vector<fo::TriRec> trirec;
+  std::vector<fo::ColRec> colrec;
+  std::vector<double> sigma;
+  bool has_A_elem = false;
+  int32_t part = 0, n_parts = 1;
+  // global footprint topology (partitioned meshes only; for the halo plan)
+  int64_t global_n_vert = 0;
+  std::vector<int32_t> global_tri;
+  std::vector<int32_t> global_part;
+  // device copies
+  fo::ColRec* d_col = nullptr;
+  fo::TriRec* d_tri = nullptr;
+  double* d_sigma = nullptr;
+  double* d_A = nullptr;           // per-wedge A^(-1/n) or nullptr
+  fo::PatchPlan plan;
+  fo::DevPatch d_plan;
+  fo_scatter scatter = FO_SCATTER_OWNER;
+  int32_t last_launches = 0;
+  // host-API staging
+  double* d_stage_U = nullptr;
+  double* d_stage_R = nullptr;
+  double* d_stage_vals = nullptr;
+  int64_t stage_vals_n = 0;
+};
+
+struct fo_graph_s {
+  fo_mesh mesh = nullptr;
+  int64_t n_rows = 0, nnz = 0;
+  int64_t* d_row_ptr = nullptr;
+  int32_t* d_col_idx = nullptr;
+};
+
+namespace fo {
+// Local topology of one footprint part (fo_host.cpp build_topology).
+struct Topo {
+  int64_t nA = 0, nB = 0, nC = 0;
+  std::vector<int64_t> glob;      // local -> global column
+  std::vector<int64_t> tri_glob;  // local -> global triangle
+  std::vector<int32_t> tri;       // local triangles (local ids)
+  std::vector<int64_t> nbr_ptr;
+  std::vector<int32_t> nbr;
+  std::vector<int64_t> colstart;
+  std::vector<TriRec> trirec;
+};
+fo_status build_topology(int64_t n_vert, int64_t n_tri, const int32_t* tri, int32_t L,
+                         const int32_t* part, int32_t my_part, Topo& T);
+void build_csr(const Topo& T, int32_t L, std::vector<int64_t>* row_ptr,
+               std::vector<int32_t>* col_idx, int64_t* nnz_out);
+void set_error(const std::string& msg);
+fo_status cuda_status(int err, const char* what);   // err: cudaError_t
+// kernels (fo_kernels.cu)
+fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* stream);
+fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_vals,
+                          void* stream);
+fo_status build_patch_plan(fo_mesh m);
+}  // namespace fo

@@ -515,6 +515,25 @@ def sub_footprint(fp: Footprint, t0: int, t1: int) -> Footprint:
                      None if fp.A_elem is None else fp.A_elem.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy())
 
 
+def sub_footprint_tris(fp: Footprint, tri_ids) -> Footprint:
+    """The triangles tri_ids (kept in ascending order) with their vertices
+    (ascending old id, so sorted neighbour lists keep their order).  Pure slicing."""
+    tri_ids = np.unique(np.asarray(tri_ids, dtype=np.int64))
+    tri = fp.tri[tri_ids]
+    verts = np.unique(tri.reshape(-1))
+    remap = -np.ones(fp.n_vert, dtype=np.int64)
+    remap[verts] = np.arange(verts.size)
+    L1 = fp.n_layers + 1
+    Uv = fp.U.reshape(fp.n_vert, L1, 2)[verts].reshape(-1).copy()
+    A = None if fp.A_elem is None else fp.A_elem.reshape(fp.n_tri, -1)[tri_ids].reshape(-1).copy()
+    sub = Footprint(fp.name + "[subset]", fp.xy[verts].copy(), remap[tri].astype(np.int32),
+                    fp.sigma.copy(), fp.thickness[verts].copy(), fp.surface[verts].copy(),
+                    None if fp.bed is None else fp.bed[verts].copy(), fp.beta[verts].copy(), Uv,
+                    dict(fp.params), A)
+    sub.vertex_ids = verts
+    return sub
+
+
 def by_name(name: str) -> Footprint:
     """workload by config id: C1, C2, C3, C4x<n>, C5."""
     if name == "C1":

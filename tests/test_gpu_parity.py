@@ -1,0 +1,201 @@
+"""GPU parity: libfo's CUDA kernels (through the C ABI) against the CPU oracle,
+element by element on the same seeded inputs:
+  residual  |R_gpu - R_ora|_inf <= 1e-12 ||M||_inf, M = sum_e |r_e| (oracle)
+  Jacobian  |dJ_ij| <= 1e-11 max_k |J_ora_ik|   (row-scaled)
+  graph     row_ptr / col_idx byte-identical.
+"""
+import numpy as np
+import pytest
+
+from paper_2204_04321_b200 import meshgen as mg
+
+pytestmark = pytest.mark.gpu
+
+R_TOL, J_TOL = 1e-12, 1e-11
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2204_04321_b200 import _build
+    _build.build()
+    return torch
+
+
+def gpu_assemble(torch, fp, params=None, scatter=None):
+    from paper_2204_04321_b200 import fo
+    mesh = fo.Mesh.from_footprint(fp, params=params)
+    if scatter is not None:
+        mesh.set_scatter(scatter)
+    U = torch.tensor(fp.U, dtype=torch.float64, device="cuda")
+    R = mesh.residual(U)
+    RJ, vals = mesh.jacobian(U)
+    torch.cuda.synchronize()
+    rp, col = mesh.graph().to_host()
+    out = dict(R=R.cpu().numpy(), RJ=RJ.cpu().numpy(), vals=vals.cpu().numpy(), row_ptr=rp, col=col,
+               mesh=mesh)
+    return out
+
+
+def check_parity(o, g, params=None, fp=None):
+    R, M, _ = o.residual(fp.U)
+    rp, col = o.graph()
+    assert g["row_ptr"].tobytes() == rp.tobytes()
+    assert g["col"].tobytes() == col.tobytes()
+    _, vals = o.jacobian(fp.U)
+    scale = np.abs(M).max() if M.size else 1.0
+    assert np.abs(g["R"] - R).max(initial=0.0) <= R_TOL * scale
+    assert np.abs(g["RJ"] - R).max(initial=0.0) <= R_TOL * scale
+    rows = np.repeat(np.arange(rp.size - 1), np.diff(rp))
+    rowmax = np.zeros(rp.size - 1)
+    np.maximum.at(rowmax, rows, np.abs(vals))
+    err = np.abs(g["vals"] - vals)
+    bad = err > J_TOL * rowmax[rows]
+    assert not bad.any(), (err[bad][:5], rowmax[rows][bad][:5], np.nonzero(bad)[0][:5])
+    return err.max(initial=0) / max(np.abs(vals).max(initial=1.0), 1e-300)
+
+
+SCATTERS = [0, 1]
+
+
+@pytest.mark.parametrize("scatter", SCATTERS)
+@pytest.mark.parametrize("case", ["C1", "gris-40km", "slab-distorted", "C5-small"])
+def test_parity_workloads(torch_cuda, ora_mod, case, scatter):
+    fp = {"C1": mg.ismip_hom_a,
+          "gris-40km": lambda: mg.greenland_like(40.0),
+          "slab-distorted": lambda: mg.slab(nx=7, n_layers=4, distort=0.25),
+          "C5-small": lambda: mg.antarctica_like(D_km=150.0, n_layers=3)}[case]()
+    if case == "C5-small":
+        fp = mg.sub_footprint(fp, 0, min(fp.n_tri, 6000))
+    g = gpu_assemble(torch_cuda, fp, scatter=scatter)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+def test_parity_c2_full(torch_cuda, ora_mod):
+    """C2 (Greenland-like 16 km, 10 layers) at its full size."""
+    fp = mg.greenland_like(16.0)
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+@pytest.mark.parametrize("params", [dict(glen_n=1.0), dict(eps_reg=0.0), dict(glen_n=2.0),
+                                    dict(A=3e-17, eps_reg=1e-6)])
+def test_parity_parameters(torch_cuda, ora_mod, params):
+    fp = mg.ismip_hom_a(nx=9, n_layers=4)
+    fp.params.update(params)
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+def test_parity_A_elem_and_floating(torch_cuda, ora_mod):
+    fp = mg.greenland_like(60.0, n_layers=6)
+    rng = mg.SplitMix64(9)
+    fp.A_elem = 1e-16 * (0.2 + 2.0 * rng.uniform(fp.n_elem))
+    assert (fp.params["rho"] * fp.thickness < -fp.params["rho_w"] * fp.bed).any()
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+@pytest.mark.parametrize("L", [1, 2, 17])
+def test_parity_layer_counts(torch_cuda, ora_mod, L):
+    fp = mg.ismip_hom_a(nx=6, n_layers=L)
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+def test_single_triangle(torch_cuda, ora_mod):
+    fp = mg.slab(nx=1, n_layers=3, distort=0.0)
+    fp = mg.sub_footprint(fp, 1, 2)
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+def test_empty_mesh(torch_cuda):
+    from paper_2204_04321_b200 import fo
+    fp = mg.ismip_hom_a(nx=2, n_layers=2)
+    fp.xy = np.zeros((0, 2)); fp.tri = np.zeros((0, 3), np.int32)
+    for a in ("thickness", "surface", "beta"):
+        setattr(fp, a, np.zeros(0))
+    fp.U = np.zeros(0)
+    mesh = fo.Mesh.from_footprint(fp)
+    assert mesh.n_dofs == 0 and mesh.n_elems == 0
+    assert mesh.graph().nnz == 0
+
+
+def test_symmetry_and_overwrite(torch_cuda):
+    """J symmetric to roundoff; outputs are overwritten, not accumulated."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like(50.0, n_layers=5)
+    mesh = fo.Mesh.from_footprint(fp)
+    U = torch.tensor(fp.U, device="cuda")
+    g = mesh.graph()
+    R = torch.full((mesh.n_dofs,), 7.0, dtype=torch.float64, device="cuda")
+    vals = torch.full((g.nnz,), -3.0, dtype=torch.float64, device="cuda")
+    mesh.jacobian(U, R=R, vals=vals)
+    R2, vals2 = mesh.jacobian(U)
+    torch.cuda.synchronize()
+    Rh, Rh2 = R.cpu().numpy(), R2.cpu().numpy()
+    sc = np.abs(Rh).max()
+    assert np.abs(Rh - Rh2).max() <= 1e-13 * sc
+    assert np.abs(vals.cpu().numpy() - vals2.cpu().numpy()).max() <= 1e-13 * np.abs(vals2.cpu().numpy()).max()
+    rp, col = g.to_host()
+    import scipy.sparse as sp
+    J = sp.csr_matrix((vals2.cpu().numpy(), col, rp), shape=(mesh.n_dofs, mesh.n_dofs))
+    assert abs(J - J.T).max() <= 1e-13 * abs(J).max()
+
+
+def test_host_buffer_entry_point(torch_cuda):
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like(50.0, n_layers=5)
+    mesh = fo.Mesh.from_footprint(fp)
+    g = mesh.graph()
+    Uh = torch.tensor(fp.U).pin_memory()
+    Rh = torch.zeros(mesh.n_dofs, dtype=torch.float64).pin_memory()
+    Vh = torch.zeros(g.nnz, dtype=torch.float64).pin_memory()
+    mesh.jacobian_host(Uh, Rh, Vh, g)
+    Rd, Vd = mesh.jacobian(torch.tensor(fp.U, device="cuda"))
+    torch.cuda.synchronize()
+    assert np.abs(Rh.numpy() - Rd.cpu().numpy()).max() <= 1e-13 * np.abs(Rh.numpy()).max()
+    assert np.abs(Vh.numpy() - Vd.cpu().numpy()).max() <= 1e-13 * np.abs(Vh.numpy()).max()
+
+
+def test_c3_full_size_sampled(torch_cuda, ora_mod):
+    """C3 at its full size in the bench's launch configuration: complete rows of
+    sampled columns vs the oracle on the sub-footprint of their triangle fans."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like_1_10()
+    mesh = fo.Mesh.from_footprint(fp)
+    U = torch.tensor(fp.U, device="cuda")
+    g = mesh.graph()
+    R, vals = mesh.jacobian(U)
+    torch.cuda.synchronize()
+    R = R.cpu().numpy()
+    rp = np.empty(g.n_rows + 1, np.int64)
+    rp, _ = g.to_host()
+    vals = vals.cpu().numpy()
+    rng = mg.SplitMix64(77)
+    cols = np.unique((rng.uniform(48) * fp.n_vert).astype(np.int64))
+    fan = np.nonzero(np.isin(fp.tri, cols).any(axis=1))[0]
+    sub = mg.sub_footprint_tris(fp, fan)
+    o = ora_mod.Oracle(sub)
+    Ro, Mo, _ = o.residual(sub.U)
+    orp, _ = o.graph()
+    _, ov = o.jacobian(sub.U)
+    L1 = fp.n_layers + 1
+    loc = {int(v): i for i, v in enumerate(sub.vertex_ids)}
+    for c in cols:
+        lc = loc[int(c)]
+        for k in range(L1):
+            for a in range(2):
+                r_g = 2 * (c * L1 + k) + a
+                r_o = 2 * (lc * L1 + k) + a
+                assert abs(R[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
+                seg_g = vals[rp[r_g]:rp[r_g + 1]]
+                seg_o = ov[orp[r_o]:orp[r_o + 1]]
+                assert seg_g.size == seg_o.size
+                assert np.abs(seg_g - seg_o).max() <= J_TOL * np.abs(seg_o).max()
