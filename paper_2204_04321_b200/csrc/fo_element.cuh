@@ -40,6 +40,7 @@ struct WedgeIn {
   double beta[3];      // basal friction (k == 0 only)
   double Afac;         // A^(-1/n)
   bool basal;
+  bool go;             // always true at run time (scheduling boundaries)
 };
 
 template <bool NEED_J, bool N3>

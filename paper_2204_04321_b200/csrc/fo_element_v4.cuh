@@ -1,0 +1,424 @@
+// fo_element_v4.cuh -- register-lean wedge element of the KA-patch kernel.
+//
+// Mathematics: the weak form of the first-order Stokes equations (PAPER.md
+// eq:FOStokes P:83-89) with the strain rates of P:90-100, Glen's law
+// eq:effvisc / eq:effeps (regularised: DESIGN.md reading L1), the
+// driving stress rho g grad s and basal linear sliding
+// on an extruded 6-node wedge; residual eq:residual and its
+// exact Jacobian eq:linearsystem.  Derivation: DESIGN.md
+// "Element math".  Same values as fo_element.cuh (the one-thread-per-wedge
+// reference formulation), reorganised so that no 12x12 accumulator set is live:
+//   1. the 6-point loop keeps per point only c = w 2mu, d = c (n-1)/(2n)/(q+eps)
+//      and the strain-rate coefficients of g = eps_a . grad phi, which is
+//      structured as g_{a,(j,l)} = f_l(zeta) P^a_j + sigma_l r_j Q^a with
+//      P^a_j = e^a_x a_j + e^a_y b_j, Q^a = e^a_z - e^a_x z_x - e^a_y z_y
+//      (stored in the caller's compact scratch `cmp`, 7 values per point);
+//   2. the frozen-viscosity part sum_q c_q H_q comes in closed form from the six
+//      c_q (moments F_ll' = sum c f_l f_l', T2_lj = sum c f_l z_x r_j, T3_jj' =
+//      sum c z_x^2 r_j r_j', ...), exact for the 3 x 2 rule;
+//   3. the rank-1 part -sum_q d_q g_q g_q^T is accumulated one 6x6 level block
+//      at a time: (bottom, top), (bottom, bottom), then (top, top) LAST, so the
+//      caller can keep the top block in registers (it becomes the next level's
+//      diagonal block after the caller's gather phase).
+// Sink interface (local DOF p = 2 j + comp of one level):
+//   r_bot_add(p, v)           residual, bottom nodes
+//   bot_add(p, p2, v)         (bottom, bottom) block, p <= p2
+//   off(p, p2, v) / off_add   (bottom, top) block (first write, then adds)
+//   top(i, v) / top_add       (top, top) block (i = pk6 packed), first write
+//   r_top(p, v) / r_top_add   top residual (first write, then adds)
+#pragma once
+
+#include "fo_element.cuh"
+
+namespace fo {
+
+__host__ __device__ constexpr int pk6(int p, int q) {
+  return p <= q ? p * 6 - (p * (p - 1)) / 2 + (q - p) : q * 6 - (q * (q - 1)) / 2 + (p - q);
+}
+
+// Compact per-point storage kept in registers (used by the reference kernels).
+struct RegCmp {
+  double v[42];
+  __device__ __forceinline__ double& operator()(int i) { return v[i]; }
+};
+
+template <bool N3, class Sink, class Cmp>
+__device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, double eps,
+                                                 double glen_n, Sink& sink, Cmp& cmp) {
+  constexpr double kZeta = 0.57735026918962576451;   // 1/sqrt(3)
+  constexpr double kTwoThirds = 2.0 / 3.0, kSixth = 1.0 / 6.0;
+  // ---- per-wedge setup (column-structured geometry)
+  double zz[3], rho[3], uz[3], vz[3];
+  double Zx0 = 0.0, Zx1 = 0.0, Zy0 = 0.0, Zy1 = 0.0;
+  double Ux0 = 0.0, Ux1 = 0.0, Uy0 = 0.0, Uy1 = 0.0;
+  double Vx0 = 0.0, Vx1 = 0.0, Vy0 = 0.0, Vy1 = 0.0;
+  {
+    double h[3], du[3], dv[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      h[j] = 0.5 * (w.zt[j] - w.zb[j]);
+      const double m = 0.5 * (w.zt[j] + w.zb[j]);
+      Zx0 = fma(w.a[j], m, Zx0); Zx1 = fma(w.a[j], h[j], Zx1);
+      Zy0 = fma(w.b[j], m, Zy0); Zy1 = fma(w.b[j], h[j], Zy1);
+      const double ubar = 0.5 * (w.ut[j] + w.ub[j]), vbar = 0.5 * (w.vt[j] + w.vb[j]);
+      du[j] = 0.5 * (w.ut[j] - w.ub[j]);
+      dv[j] = 0.5 * (w.vt[j] - w.vb[j]);
+      Ux0 = fma(w.a[j], ubar, Ux0); Ux1 = fma(w.a[j], du[j], Ux1);
+      Uy0 = fma(w.b[j], ubar, Uy0); Uy1 = fma(w.b[j], du[j], Uy1);
+      Vx0 = fma(w.a[j], vbar, Vx0); Vx1 = fma(w.a[j], dv[j], Vx1);
+      Vy0 = fma(w.b[j], vbar, Vy0); Vy1 = fma(w.b[j], dv[j], Vy1);
+    }
+    const double hs = h[0] + h[1] + h[2];
+    const double dus = du[0] + du[1] + du[2], dvs = dv[0] + dv[1] + dv[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      zz[a] = (3.0 * h[a] + hs) * kSixth;           // z_zeta at triangle point a
+      const double izz = 1.0 / zz[a];
+      rho[a] = 0.5 * izz;                           // r_j(a) = L_j(a) rho_a
+      uz[a] = (3.0 * du[a] + dus) * kSixth * izz;   // u_z at point a
+      vz[a] = (3.0 * dv[a] + dvs) * kSixth * izz;
+    }
+  }
+  const double W0 = w.D * kSixth;   // quadrature weight 1/6 x det, det = 2|T| z_zeta
+  // ---- driving stress rho g grad s . int phi (reading L10), bottom half, and
+  //      the basal friction term (readings L6-L8) on layer 0
+  {
+    const double zs = zz[0] + zz[1] + zz[2];
+    double rb[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double bj = rg * W0 * (3.0 * zz[j] + zs) * kSixth;
+      rb[2 * j] = w.sx * bj;
+      rb[2 * j + 1] = w.sy * bj;
+      sink.r_top(2 * j, w.sx * bj);
+      sink.r_top(2 * j + 1, w.sy * bj);
+    }
+    if (w.basal) {
+      const double dz1 = w.zb[1] - w.zb[0], dz2 = w.zb[2] - w.zb[0];
+      const double cxp = w.e1y * dz2 - dz1 * w.e2y;
+      const double cyp = dz1 * w.e2x - w.e1x * dz2;
+      const double wb = (1.0 / 6.0) * sqrt(cxp * cxp + cyp * cyp + w.D * w.D);   // |T3D| / 3
+      double Mb[3][3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int j2 = 0; j2 < 3; ++j2) Mb[j][j2] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double La[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) La[j] = j == a ? kTwoThirds : kSixth;
+        const double bq = wb * (La[0] * w.beta[0] + La[1] * w.beta[1] + La[2] * w.beta[2]);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+          for (int j2 = 0; j2 < 3; ++j2) Mb[j][j2] = fma(bq * La[j], La[j2], Mb[j][j2]);
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        rb[2 * j] = fma(Mb[j][0], w.ub[0], fma(Mb[j][1], w.ub[1], fma(Mb[j][2], w.ub[2], rb[2 * j])));
+        rb[2 * j + 1] = fma(Mb[j][0], w.vb[0], fma(Mb[j][1], w.vb[1], fma(Mb[j][2], w.vb[2], rb[2 * j + 1])));
+#pragma unroll
+        for (int j2 = j; j2 < 3; ++j2) {
+          sink.bot_add(2 * j, 2 * j2, Mb[j][j2]);
+          sink.bot_add(2 * j + 1, 2 * j2 + 1, Mb[j][j2]);
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 6; ++p) sink.r_bot_add(p, rb[p]);
+  }
+  // ---- quadrature loop: compact per-point data
+  double cq[6];
+#define dq(q) cmp(7 * (q) + 0)
+#define E1x(q) cmp(7 * (q) + 1)
+#define E1y(q) cmp(7 * (q) + 2)
+#define Qu(q) cmp(7 * (q) + 3)
+#define E2x(q) cmp(7 * (q) + 4)
+#define E2y(q) cmp(7 * (q) + 5)
+#define Qv(q) cmp(7 * (q) + 6)
+  {
+    const double ex1 = (1.0 - glen_n) / (2.0 * glen_n);
+    const double kap = (glen_n - 1.0) / (2.0 * glen_n);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int q = 2 * a + s;
+        const double zeta = s == 0 ? -kZeta : kZeta;
+        const double zx = fma(zeta, Zx1, Zx0), zy = fma(zeta, Zy1, Zy0);
+        const double ux = fma(zeta, Ux1, Ux0) - zx * uz[a];
+        const double uy = fma(zeta, Uy1, Uy0) - zy * uz[a];
+        const double vx = fma(zeta, Vx1, Vx0) - zx * vz[a];
+        const double vy = fma(zeta, Vy1, Vy0) - zy * vz[a];
+        const double exy = 0.5 * (uy + vx), exz = 0.5 * uz[a], eyz = 0.5 * vz[a];
+        // effective strain rate squared, eq:effeps
+        const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
+        const double qe = qq + eps;
+        const double W = W0 * zz[a];
+        double c, d;
+        if (N3) {
+          const double y = rcbrt(qe);                  // (q + eps)^(-1/3)
+          c = W * w.Afac * y;                           // w_q 2 mu_q
+          d = c * (y * y * y) * (1.0 / 3.0);            // c (n-1)/(2n) / (q+eps)
+        } else {
+          c = W * w.Afac * pow(qe, ex1);
+          d = c * kap / qe;
+        }
+        // strain-rate vectors
+        const double e1x = 2.0 * ux + vy, e1y = exy, e1z = exz;
+        const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
+        Qu(q) = e1z - e1x * zx - e1y * zy;
+        Qv(q) = e2z - e2x * zx - e2y * zy;
+        E1x(q) = e1x; E1y(q) = e1y; E2x(q) = e2x; E2y(q) = e2y;
+        cq[q] = c;
+        dq(q) = d;
+      }
+    }
+  }
+  // ---- viscous residual R_{a,(j,l)} = sum_q c_q (f_l P^a_j + sigma_l r_j Q^a)
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    double ub = 0.0, vb = 0.0, ut = 0.0, vt = 0.0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int a = q >> 1;
+      const double f0 = (q & 1) ? 0.5 - 0.5 * kZeta : 0.5 + 0.5 * kZeta;
+      const double crj = cq[q] * ((j == a) ? kTwoThirds : kSixth) * rho[a];
+      const double cpu = cq[q] * fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
+      const double cpv = cq[q] * fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
+      ub = fma(f0, cpu, fma(-crj, Qu(q), ub));
+      vb = fma(f0, cpv, fma(-crj, Qv(q), vb));
+      ut = fma(1.0 - f0, cpu, fma(crj, Qu(q), ut));
+      vt = fma(1.0 - f0, cpv, fma(crj, Qv(q), vt));
+    }
+    sink.r_bot_add(2 * j, ub);
+    sink.r_bot_add(2 * j + 1, vb);
+    sink.r_top_add(2 * j, ut);
+    sink.r_top_add(2 * j + 1, vt);
+  }
+  // ---- frozen-viscosity part in closed form from the six c_q
+  double F[3];                        // F_00, F_01, F_11 = sum c f_l f_l'
+  double T2x[2][3], T2y[2][3];        // sum c f_l z_x r_j, sum c f_l z_y r_j
+  double KKuu[6], KKvv[6], KKuv[6];   // z- and z_x z_y-moment combinations, packed j <= j'
+  {
+    double S[3], Dd[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      S[a] = cq[2 * a] + cq[2 * a + 1];
+      Dd[a] = kZeta * (cq[2 * a + 1] - cq[2 * a]);
+    }
+    const double St = S[0] + S[1] + S[2], Dt = Dd[0] + Dd[1] + Dd[2];
+    F[0] = St * (1.0 / 3.0) - 0.5 * Dt;
+    F[1] = St * kSixth;
+    F[2] = St * (1.0 / 3.0) + 0.5 * Dt;
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const double sg = l == 0 ? -1.0 : 1.0;
+      double Yx[3], Yy[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double s3 = S[a] * (1.0 / 3.0);
+        Yx[a] = rho[a] * 0.5 * fma(Zx0, S[a], fma(Zx1 + sg * Zx0, Dd[a], sg * Zx1 * s3));
+        Yy[a] = rho[a] * 0.5 * fma(Zy0, S[a], fma(Zy1 + sg * Zy0, Dd[a], sg * Zy1 * s3));
+      }
+      const double sx6 = (Yx[0] + Yx[1] + Yx[2]) * kSixth, sy6 = (Yy[0] + Yy[1] + Yy[2]) * kSixth;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        T2x[l][j] = fma(0.5, Yx[j], sx6);   // sum_a L_j(a) Y_a
+        T2y[l][j] = fma(0.5, Yy[j], sy6);
+      }
+    }
+    double ku[3], kv[3], kuv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double s3 = S[a] * (1.0 / 3.0);
+      const double XXx = fma(Zx0 * Zx0, S[a], fma(2.0 * Zx0 * Zx1, Dd[a], Zx1 * Zx1 * s3));
+      const double XXy = fma(Zy0 * Zy0, S[a], fma(2.0 * Zy0 * Zy1, Dd[a], Zy1 * Zy1 * s3));
+      const double XXxy = fma(Zx0 * Zy0, S[a], fma(fma(Zx0, Zy1, Zx1 * Zy0), Dd[a], Zx1 * Zy1 * s3));
+      const double r2 = rho[a] * rho[a];
+      ku[a] = r2 * fma(2.0, XXx, 0.5 * (XXy + S[a]));
+      kv[a] = r2 * fma(2.0, XXy, 0.5 * (XXx + S[a]));
+      kuv[a] = r2 * 1.5 * XXxy;
+    }
+    // T3_jj' = sum_a L_j(a) L_j'(a) kappa_a
+    const double su = (ku[0] + ku[1] + ku[2]) * (1.0 / 36.0);
+    const double sv = (kv[0] + kv[1] + kv[2]) * (1.0 / 36.0);
+    const double suv = (kuv[0] + kuv[1] + kuv[2]) * (1.0 / 36.0);
+    int i = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int j2 = j; j2 < 3; ++j2) {
+        const double wj = j == j2 ? 15.0 / 36.0 : 3.0 / 36.0;
+        const double pu = j == j2 ? ku[j] : ku[j] + ku[j2];
+        const double pv = j == j2 ? kv[j] : kv[j] + kv[j2];
+        const double puv = j == j2 ? kuv[j] : kuv[j] + kuv[j2];
+        KKuu[i] = fma(wj, pu, su);
+        KKvv[i] = fma(wj, pv, sv);
+        KKuv[i] = fma(wj, puv, suv);
+        ++i;
+      }
+  }
+  // frozen-viscosity entry: row comp ca of node (j,l), column comp cb of node (j2,l2)
+  auto hpart = [&](int ca, int j, int l, int cb, int j2, int l2) -> double {
+    const double sg = l == 0 ? -1.0 : 1.0, sg2 = l2 == 0 ? -1.0 : 1.0;
+    const double Fv = F[l + l2];
+    const int kk = j <= j2 ? (j * 3 - (j * (j - 1)) / 2 + (j2 - j)) : (j2 * 3 - (j2 * (j2 - 1)) / 2 + (j - j2));
+    const double aj = w.a[j], bj = w.b[j], aj2 = w.a[j2], bj2 = w.b[j2];
+    if (ca == 0 && cb == 0) {
+      const double AA = fma(2.0 * aj, aj2, 0.5 * bj * bj2);
+      const double G1 = fma(2.0 * aj, T2x[l][j2], 0.5 * bj * T2y[l][j2]);
+      const double G2 = fma(2.0 * aj2, T2x[l2][j], 0.5 * bj2 * T2y[l2][j]);
+      return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKuu[kk])));
+    } else if (ca == 1 && cb == 1) {
+      const double AA = fma(0.5 * aj, aj2, 2.0 * bj * bj2);
+      const double G1 = fma(0.5 * aj, T2x[l][j2], 2.0 * bj * T2y[l][j2]);
+      const double G2 = fma(0.5 * aj2, T2x[l2][j], 2.0 * bj2 * T2y[l2][j]);
+      return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKvv[kk])));
+    } else if (ca == 0) {   // row u(j,l), column v(j2,l2)
+      const double AA = fma(aj, bj2, 0.5 * aj2 * bj);
+      const double G1 = fma(aj, T2y[l][j2], 0.5 * bj * T2x[l][j2]);
+      const double G2 = fma(bj2, T2x[l2][j], 0.5 * aj2 * T2y[l2][j]);
+      return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKuv[kk])));
+    } else {                // row v(j,l), column u(j2,l2) = J_{u(j2,l2), v(j,l)}
+      const double AA = fma(aj2, bj, 0.5 * aj * bj2);
+      const double G1 = fma(aj2, T2y[l2][j], 0.5 * bj2 * T2x[l2][j]);
+      const double G2 = fma(bj, T2x[l][j2], 0.5 * aj * T2y[l][j2]);
+      return fma(Fv, AA, fma(-sg, G1, fma(-sg2, G2, sg * sg2 * KKuv[kk])));
+    }
+  };
+  // The sections below are wrapped in `if (w.go)` (always true at run time):
+  // branch boundaries keep ptxas from interleaving them, and each rank-1
+  // block reads d_q as fma(0, gate, d_q) with gate = a result of the previous
+  // section (an IEEE-exact no-op that orders the blocks), so one accumulator
+  // set is live at a time.
+  double gate = 0.0;
+  if (w.go) {   // frozen-viscosity (top, top): first writes of the held block
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2) {
+        const double v = hpart(p & 1, p >> 1, 1, p2 & 1, p2 >> 1, 1);
+        sink.top(pk6(p, p2), v);
+        gate = v;
+      }
+  }
+  if (w.go) {   // frozen-viscosity (bottom, top): first writes
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = 0; p2 < 6; ++p2) {
+        const double v = hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 1);
+        sink.off(p, p2, v);
+        gate = v;
+      }
+  }
+  if (w.go) {   // frozen-viscosity (bottom, bottom)
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2) sink.bot_add(p, p2, hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 0));
+  }
+  if (w.go) {   // rank-1 (bottom, top)
+    double acc[36];
+#pragma unroll
+    for (int i = 0; i < 36; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+      const int a = q >> 1;
+      const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
+      const double zeta = (q & 1) ? kZeta : -kZeta;
+      const double f0 = 0.5 - 0.5 * zeta, f1 = 0.5 + 0.5 * zeta;
+      const double dg = fma(0.0, gate, dq(q));
+      double gb[6], gt[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
+        const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
+        const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
+        gb[2 * j] = dg * fma(f0, pu, -rj * Qu(q));
+        gb[2 * j + 1] = dg * fma(f0, pv, -rj * Qv(q));
+        gt[2 * j] = fma(f1, pu, rj * Qu(q));
+        gt[2 * j + 1] = fma(f1, pv, rj * Qv(q));
+      }
+#pragma unroll
+      for (int p = 0; p < 6; ++p)
+#pragma unroll
+        for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = fma(-gb[p], gt[p2], acc[6 * p + p2]);
+    }
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = 0; p2 < 6; ++p2) sink.off_add(p, p2, acc[6 * p + p2]);
+    gate = acc[35];
+  }
+  if (w.go) {   // rank-1 (bottom, bottom)
+    double acc[21];
+#pragma unroll
+    for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+      const int a = q >> 1;
+      const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
+      const double zeta = (q & 1) ? kZeta : -kZeta;
+      const double f0 = 0.5 - 0.5 * zeta;
+      const double dd = fma(0.0, gate, dq(q));
+      double g[6], dg[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
+        g[2 * j] = fma(f0, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), -rj * Qu(q));
+        g[2 * j + 1] = fma(f0, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), -rj * Qv(q));
+      }
+#pragma unroll
+      for (int p = 0; p < 6; ++p) dg[p] = dd * g[p];
+#pragma unroll
+      for (int p = 0; p < 6; ++p)
+#pragma unroll
+        for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = fma(-dg[p], g[p2], acc[pk6(p, p2)]);
+    }
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2) sink.bot_add(p, p2, acc[pk6(p, p2)]);
+    gate = acc[20];
+  }
+  if (w.go) {   // rank-1 (top, top), added to the held block
+    double acc[21];
+#pragma unroll
+    for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+      const int a = q >> 1;
+      const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
+      const double zeta = (q & 1) ? kZeta : -kZeta;
+      const double f1 = 0.5 + 0.5 * zeta;
+      const double dd = fma(0.0, gate, dq(q));
+      double g[6], dg[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
+        g[2 * j] = fma(f1, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), rj * Qu(q));
+        g[2 * j + 1] = fma(f1, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), rj * Qv(q));
+      }
+#pragma unroll
+      for (int p = 0; p < 6; ++p) dg[p] = dd * g[p];
+#pragma unroll
+      for (int p = 0; p < 6; ++p)
+#pragma unroll
+        for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = fma(-dg[p], g[p2], acc[pk6(p, p2)]);
+    }
+#pragma unroll
+    for (int i = 0; i < 21; ++i) sink.top_add(i, acc[i]);
+  }
+#undef dq
+#undef E1x
+#undef E1y
+#undef Qu
+#undef E2x
+#undef E2y
+#undef Qv
+}
+
+}  // namespace fo

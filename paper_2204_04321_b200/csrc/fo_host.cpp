@@ -559,14 +559,18 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_tri);
   cudaFree(m->d_sigma);
   cudaFree(m->d_A);
-  cudaFree(m->d_plan.col_begin);
-  cudaFree(m->d_plan.tri_ptr);
-  cudaFree(m->d_plan.tri_list);
-  cudaFree(m->d_plan.inc_ptr);
-  cudaFree(m->d_plan.inc);
+  cudaFree(m->d_plan.t_begin);
+  cudaFree(m->d_plan.col_ptr);
+  cudaFree(m->d_plan.pair_ptr);
+  cudaFree(m->d_plan.contrib_ptr);
+  cudaFree(m->d_plan.cols);
+  cudaFree(m->d_plan.pairs);
+  cudaFree(m->d_plan.contrib);
+  cudaFree(m->d_plan.zero_cols);
   cudaFree(m->d_stage_U);
   cudaFree(m->d_stage_R);
   cudaFree(m->d_stage_vals);
+  cudaFree(m->d_scratch_R);
   delete m;
 }
 

@@ -27,26 +27,52 @@ struct alignas(8) TriRec {
   uint8_t pad[3];
 };
 
-// Column-patch work decomposition of the owner-computes kernel.
+// Triangles per patch of the owner-computes kernel (one thread per triangle
+// column, 105 fp64 of shared memory per triangle).
+constexpr int kPatchTris = 240;
+// shared-memory budget of one patch's plan (columns, pairs, contributions)
+constexpr int kPlanBytes = 232448 - 105 * kPatchTris * 8 - 256;
+
+// plan records (fo_plan.cpp); copied to shared memory by the kernel
+struct PlanCol {            // 24 bytes
+  int64_t colstart;         // CSR value offset of the column's first row
+  int32_t c;                // local column id
+  int32_t info;             // n_c | interior << 8 | self slot << 9
+  uint16_t self_off;        // contributions of the self slot (residual)
+  uint16_t self_cnt;
+  uint32_t pad;
+};
+struct PlanPair {           // 8 bytes: one (column, slot) of phase B
+  uint16_t off;             // first contribution (patch-relative)
+  uint8_t cnt;              // number of contributions
+  uint8_t slot;             // slot in the column's coupling list
+  uint16_t col;             // patch-local column record
+  uint16_t pad;
+};
+
+// Work decomposition of the owner-computes kernel.
 struct PatchPlan {
   int32_t n_patches = 0;
-  int32_t max_tris = 0;          // max triangles of any patch (block capacity)
-  int32_t max_cols = 0;
-  std::vector<int32_t> col_begin;  // [n_patches+1] owned-column range of patch p
-  std::vector<int32_t> tri_ptr;    // [n_patches+1] into tri_list
-  std::vector<int32_t> tri_list;   // local triangle ids touching the patch's columns
-  // per patch-column incidence: for owned column c of patch p, the list of
-  // (patch-local triangle index << 2 | local vertex index of c) entries
-  std::vector<int32_t> inc_ptr;    // [n_owned_cols+1] global (over all patches)
-  std::vector<int32_t> inc;        // packed entries
+  int64_t max_plan_bytes = 0;
+  std::vector<int32_t> t_begin;      // [n_patches+1] triangle range of patch p
+  std::vector<int32_t> col_ptr;      // [n_patches+1]
+  std::vector<int32_t> pair_ptr;     // [n_patches+1]
+  std::vector<int64_t> contrib_ptr;  // [n_patches+1]
+  std::vector<PlanCol> cols;
+  std::vector<PlanPair> pairs;
+  std::vector<uint16_t> contrib;     // tl << 4 | j << 2 | j'
+  std::vector<int32_t> zero_cols;    // boundary columns (zero-filled before the kernel)
 };
 
 struct DevPatch {
-  int32_t* col_begin = nullptr;
-  int32_t* tri_ptr = nullptr;
-  int32_t* tri_list = nullptr;
-  int32_t* inc_ptr = nullptr;
-  int32_t* inc = nullptr;
+  int32_t* t_begin = nullptr;
+  int32_t* col_ptr = nullptr;
+  int32_t* pair_ptr = nullptr;
+  int64_t* contrib_ptr = nullptr;
+  PlanCol* cols = nullptr;
+  PlanPair* pairs = nullptr;
+  uint16_t* contrib = nullptr;
+  int32_t* zero_cols = nullptr;
 };
 
 }  // namespace fo
@@ -88,6 +114,7 @@ struct fo_mesh_s {
   double* d_stage_U = nullptr;
   double* d_stage_R = nullptr;
   double* d_stage_vals = nullptr;
+  double* d_scratch_R = nullptr;   // residual scratch when the caller passes no R
   int64_t stage_vals_n = 0;
 };
 

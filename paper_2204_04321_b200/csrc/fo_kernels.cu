@@ -88,10 +88,7 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
-    st = launch_owner(m, d_U, d_R, nullptr, s);
-    if (st) return st;
-    m->last_launches = 1;
-    return FO_OK;
+    return launch_owner(m, d_U, d_R, nullptr, s);
   }
   st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
   if (st) return st;
@@ -109,10 +106,7 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
-    st = launch_owner(m, d_U, d_R, d_vals, s);
-    if (st) return st;
-    m->last_launches = 1;
-    return FO_OK;
+    return launch_owner(m, d_U, d_R, d_vals, s);
   }
   if (d_R) st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
   if (!st && m->nnz > 0)

@@ -15,6 +15,7 @@ struct KParams {
   double eps;         // eps_reg
   double glen_n;      // n
   double Afac;        // A^(-1/n) when no per-wedge field
+  int go;             // 1 (opaque to the compiler)
 };
 
 inline KParams make_kparams(fo_mesh m) {
@@ -25,6 +26,7 @@ inline KParams make_kparams(fo_mesh m) {
   kp.eps = m->p.eps_reg;
   kp.glen_n = m->p.glen_n;
   kp.Afac = pow(m->p.A, -1.0 / m->p.glen_n);
+  kp.go = 1;
   return kp;
 }
 
@@ -77,7 +79,7 @@ __device__ __forceinline__ TriRec load_tri(const TriRec* __restrict__ tris, int6
 __device__ __forceinline__ void wedge_input(const TriGeo& g, const TriRec& tr,
                                             const double* __restrict__ sigma, double Afac,
                                             const double* __restrict__ U, int L, int k,
-                                            WedgeIn& w) {
+                                            WedgeIn& w, bool go = true) {
   const double sk = __ldg(sigma + k), sk1 = __ldg(sigma + k + 1);
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -94,6 +96,7 @@ __device__ __forceinline__ void wedge_input(const TriGeo& g, const TriRec& tr,
   w.sx = g.sx; w.sy = g.sy;
   w.Afac = Afac;
   w.basal = (k == 0);
+  w.go = go;
 }
 
 // convenience for the one-thread-per-wedge kernels

@@ -1,7 +1,362 @@
-// fo_owner.cu -- placeholder, replaced by the patch kernel
+// fo_owner.cu -- KA-patch: owner-computes residual (+ Jacobian) assembly
+// (DESIGN.md "KA-patch").  PAPER.md P:177-183 (gather, interpolate,
+// evaluate, scatter) fused into one kernel; the scatter writes every CSR value
+// of an interior column exactly once with coalesced plain stores (the
+// overwrite semantics of fo_assemble_jacobian), boundary columns with RED.
+//
+// One CTA = one patch of <= kPatchTris consecutive triangles, one thread per
+// triangle column, layers k = 0..L-1 in order.  Per layer:
+//   phase A  each thread evaluates wedge (t,k) in registers (fo_element.cuh)
+//            and publishes to shared memory (SoA, [entry][triangle]):
+//              D  += bottom-bottom block + bottom residual  (D already holds
+//                    the top-top block + top residual of wedge k-1: the
+//                    vertical merge of the shared level k)
+//              O[k&1] = bottom-top block (rows level k, columns level k+1)
+//   phase B  every warp takes whole columns of the patch; lanes walk the
+//            contiguous level-k segment of the column's two rows (u, v) and
+//            gather each double2 (b = 0,1) from D / O[k&1] / O[(k-1)&1]^T
+//            through the plan's per-slot contribution lists.
+//   then the thread stores its held top-top block into D for layer k+1.
+// A final phase B writes the surface level L.
+#include <cuda_runtime.h>
+
+#include "fo_element.cuh"
+#include "fo_element_v4.cuh"
+
+#include <type_traits>
+#include "fo_internal.h"
 #include "fo_kernels.cuh"
+
 namespace fo {
-fo_status build_patch_plan(fo_mesh m) { m->plan.n_patches = 0; m->scatter = FO_SCATTER_ATOMIC; return FO_OK; }
-fo_status launch_owner(fo_mesh, const double*, double*, double*, cudaStream_t) {
-  set_error("owner kernel not built"); return FO_ESTATE; }
+
+struct PlanView {
+  const int32_t* __restrict__ t_begin;
+  const int32_t* __restrict__ col_ptr;
+  const int32_t* __restrict__ pair_ptr;
+  const int64_t* __restrict__ contrib_ptr;
+  const PlanCol* __restrict__ cols;
+  const PlanPair* __restrict__ pairs;
+  const uint16_t* __restrict__ contrib;
+};
+
+constexpr int TP = kPatchTris;
+constexpr int kD = 27;   // level-k diagonal block (21, 2x2-block layout) + 6 residual
+constexpr int kO = 36;   // 6x6 bottom-top block of wedge k
+constexpr int kC = 42;   // compact per-point scratch (7 x 6 quadrature points)
+constexpr int kSlotsPerTri = kD + kO + kC;
+
+// D layout: the three off-diagonal 2x2 node blocks (j < j2) first, row-major
+// [a][b], at 4 (j + j2 - 1); then the three diagonal node blocks (a <= b) at
+// 12 + 3 j + a + b; the residual at 21 + 2 j + a.
+__host__ __device__ constexpr int dmap(int p, int p2) {
+  return (p >> 1) == (p2 >> 1) ? 12 + 3 * (p >> 1) + (p & 1) + (p2 & 1)
+                               : 4 * ((p >> 1) + (p2 >> 1) - 1) + 2 * (p & 1) + (p2 & 1);
 }
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// The patch's plan in shared memory.
+struct SmemPlan {
+  const PlanCol* cols;
+  const PlanPair* pairs;
+  const uint16_t* contrib;
+  int ncols, npairs;
+};
+
+__device__ __forceinline__ void put2(double* dst, double x, double y, bool interior) {
+  if (interior) {
+    *reinterpret_cast<double2*>(dst) = make_double2(x, y);
+  } else {
+    red_add(dst, x);
+    red_add(dst + 1, y);
+  }
+}
+
+// Phase B for wedge layer k (kk = k < L) or the surface (kk = L, D only).
+// One thread per (column, slot) pair walks the slot's contributions once and
+// gathers: level-kk rows, column level kk (from D) and kk+1 (from O); level
+// kk+1 rows, column level kk (from O transposed).  The level-kk rows' column
+// level kk-1 part was written by the previous call (partial rows, merged in
+// L2).  The self slot also gathers the residual of node (c, kk).
+template <bool NEED_J>
+__device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const double* D,
+                                        const double* O, double* __restrict__ R,
+                                        double* __restrict__ vals) {
+  const bool has_up = kk < L;
+  const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // groups of level-kk rows
+  const int m1 = (kk + 1 == L) ? 2 : 3;                   // groups of level-kk+1 rows
+  const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
+  const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk row slot
+  if (!NEED_J) {
+    for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
+      const PlanCol& pc = sp.cols[ci];
+      double r0 = 0.0, r1 = 0.0;
+      for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; ++e) {
+        const int cb = sp.contrib[e];
+        const int tl = cb >> 4, j = (cb >> 2) & 3;
+        r0 += D[(21 + 2 * j) * TP + tl];
+        r1 += D[(22 + 2 * j) * TP + tl];
+      }
+      put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
+    }
+    return;
+  }
+  for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
+    const PlanPair pp = sp.pairs[pi];
+    const PlanCol& pc = sp.cols[pp.col];
+    const int nc = pc.info & 255;
+    const bool interior = (pc.info >> 8) & 1;
+    const bool is_self = pp.slot == ((pc.info >> 9) & 255);
+    double dg[2][2], up[2][2], nx[2][2], rr[2] = {0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dg[a][b] = up[a][b] = nx[a][b] = 0.0;
+    for (int e = pp.off; e < pp.off + pp.cnt; ++e) {
+      const int cb = sp.contrib[e];
+      const int tl = cb >> 4, j = (cb >> 2) & 3, j2 = cb & 3;
+      int dbase, sa, sb;
+      if (j == j2) { dbase = 12 + 3 * j; sa = 1; sb = 1; }
+      else { dbase = 4 * (j + j2 - 1); sa = j < j2 ? 2 : 1; sb = j < j2 ? 1 : 2; }
+      const double* Dt = D + tl;
+      const double* Ot = O + tl;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          dg[a][b] += Dt[(dbase + sa * a + sb * b) * TP];
+          if (has_up) {
+            up[a][b] += Ot[(6 * (2 * j + a) + 2 * j2 + b) * TP];
+            nx[a][b] += Ot[(6 * (2 * j2 + b) + 2 * j + a) * TP];
+          }
+        }
+      if (is_self) {
+        rr[0] += Dt[(21 + 2 * j) * TP];
+        rr[1] += Dt[(22 + 2 * j) * TP];
+      }
+    }
+    if (!interior && pp.cnt == 0) continue;
+    const int64_t seg0 = pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      double* d0 = vals + seg0 + int64_t(a) * (2 * nc * m0);
+      put2(d0, dg[a][0], dg[a][1], interior);
+      if (has_up) put2(d0 + 2, up[a][0], up[a][1], interior);
+    }
+    if (has_up) {
+      const int64_t seg1 = pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
+#pragma unroll
+      for (int a = 0; a < 2; ++a) put2(vals + seg1 + int64_t(a) * (2 * nc * m1), nx[a][0], nx[a][1], interior);
+    }
+    if (is_self) put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), rr[0], rr[1], interior);
+  }
+}
+
+// Sink of wedge_element_v4: bottom parts added to D and O in shared memory,
+// the top (level k+1) block and residual held in registers.
+struct PatchSink {
+  double* D;
+  double* O;
+  int tl;
+  double held[27];   // dmap layout
+  __device__ __forceinline__ void r_bot_add(int p, double v) { D[(21 + p) * TP + tl] += v; }
+  __device__ __forceinline__ void bot_add(int p, int p2, double v) { D[dmap(p, p2) * TP + tl] += v; }
+  __device__ __forceinline__ void off(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] = v; }
+  __device__ __forceinline__ void off_add(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] += v; }
+  __device__ __forceinline__ void top(int i, double v) {
+    // i is the packed upper-triangle index pk6(p, p2)
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2)
+        if (pk6(p, p2) == i) held[dmap(p, p2)] = v;
+  }
+  __device__ __forceinline__ void top_add(int i, double v) {
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2)
+        if (pk6(p, p2) == i) held[dmap(p, p2)] += v;
+  }
+  __device__ __forceinline__ void r_top(int p, double v) { held[21 + p] = v; }
+  __device__ __forceinline__ void r_top_add(int p, double v) { held[21 + p] += v; }
+};
+
+// residual-only sink: the Jacobian parts of the element are dead code
+struct PatchSinkR {
+  double* D;
+  int tl;
+  double held[27];
+  __device__ __forceinline__ void r_bot_add(int p, double v) { D[(21 + p) * TP + tl] += v; }
+  __device__ __forceinline__ void bot_add(int, int, double) {}
+  __device__ __forceinline__ void off(int, int, double) {}
+  __device__ __forceinline__ void off_add(int, int, double) {}
+  __device__ __forceinline__ void top(int, double) {}
+  __device__ __forceinline__ void top_add(int, double) {}
+  __device__ __forceinline__ void r_top(int p, double v) { held[21 + p] = v; }
+  __device__ __forceinline__ void r_top_add(int p, double v) { held[21 + p] += v; }
+};
+
+// the thread's compact per-point scratch: 42 doubles at base[i * TP + tl]
+struct SmemCmp {
+  double* base;
+  int tl;
+  __device__ __forceinline__ double& operator()(int i) { return base[i * TP + tl]; }
+};
+
+template <bool NEED_J, bool N3>
+__global__ void __launch_bounds__(TP, 1)
+ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
+                const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
+                PlanView pv, const double* __restrict__ U, double* __restrict__ R,
+                double* __restrict__ vals) {
+  extern __shared__ double smem[];
+  double* const D = smem;                    // [kD][TP]
+  double* const O = smem + kD * TP;          // [kO][TP]
+  double* const C = smem + (kD + kO) * TP;   // [kC][TP]
+  const int p = blockIdx.x;
+  const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
+  // the patch's plan -> shared memory (after the value buffers)
+  SmemPlan sp;
+  {
+    const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
+    const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
+    const int64_t e0 = __ldg(pv.contrib_ptr + p), e1 = __ldg(pv.contrib_ptr + p + 1);
+    char* base = reinterpret_cast<char*>(smem + kSlotsPerTri * TP);
+    PlanCol* cs = reinterpret_cast<PlanCol*>(base);
+    PlanPair* ps = reinterpret_cast<PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
+    uint16_t* es = reinterpret_cast<uint16_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
+    for (int i = threadIdx.x; i < (c1 - c0) * int(sizeof(PlanCol) / 8); i += blockDim.x)
+      reinterpret_cast<int2*>(cs)[i] = __ldg(reinterpret_cast<const int2*>(pv.cols + c0) + i);
+    for (int i = threadIdx.x; i < q1 - q0; i += blockDim.x)
+      reinterpret_cast<int2*>(ps)[i] = __ldg(reinterpret_cast<const int2*>(pv.pairs + q0) + i);
+    for (int i = threadIdx.x; i < int(e1 - e0); i += blockDim.x) es[i] = __ldg(pv.contrib + e0 + i);
+    sp.cols = cs; sp.pairs = ps; sp.contrib = es;
+    sp.ncols = c1 - c0; sp.npairs = q1 - q0;
+  }
+  const int L = kp.L;
+  const int tl = threadIdx.x;
+  const bool active = tl < nt;
+  TriRec tr;
+  tr.v[0] = tr.v[1] = tr.v[2] = 0;
+  if (active) {
+    const int* tp = reinterpret_cast<const int*>(tris + (t0 + tl));
+    const int2 v01 = __ldg(reinterpret_cast<const int2*>(tp));
+    tr.v[0] = v01.x; tr.v[1] = v01.y; tr.v[2] = __ldg(tp + 2);
+#pragma unroll
+    for (int i = 0; i < kD; ++i) D[i * TP + tl] = 0.0;
+  }
+  for (int k = 0; k < L; ++k) {
+    typename std::conditional<NEED_J, PatchSink, PatchSinkR>::type sk;
+    sk.D = D;
+    sk.tl = tl;
+    if constexpr (NEED_J) sk.O = O;
+    if (active) {
+      // re-gather the (L1-resident) column records every layer instead of
+      // keeping ~60 registers of triangle geometry live across the layer loop
+      const ColRec* colk = col;
+      asm volatile("" : "+l"(colk));
+      TriGeo geo;
+      load_tri_geo(colk, tr, geo);
+      const double Afac = Aw ? __ldg(Aw + int64_t(t0 + tl) * L + k) : kp.Afac;
+      WedgeIn w;
+      wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
+      SmemCmp cmp{C, tl};
+      wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
+    }
+    __syncthreads();
+    phase_b<NEED_J>(sp, k, L, D, O, R, vals);
+    __syncthreads();
+    if (active) {   // the held top block becomes level k+1's diagonal block
+      if (NEED_J) {
+#pragma unroll
+        for (int i = 0; i < kD; ++i) D[i * TP + tl] = sk.held[i];
+      } else {
+#pragma unroll
+        for (int i = 21; i < kD; ++i) D[i * TP + tl] = sk.held[i];
+      }
+    }
+  }
+  __syncthreads();
+  phase_b<NEED_J>(sp, L, L, D, O, R, vals);
+}
+
+// zero the rows (CSR values and residual) of boundary columns
+__global__ void zero_boundary_kernel(const ColRec* __restrict__ col, const int32_t* __restrict__ zc,
+                                     int n, int L, double* __restrict__ R, double* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+    const int c = zc[w];
+    if (R)
+      for (int i = lane; i < 2 * (L + 1); i += 32) R[2 * int64_t(c) * (L + 1) + i] = 0.0;
+    if (vals) {
+      const long long csn = __double_as_longlong(__ldg(reinterpret_cast<const double*>(col + c) + 5));
+      const int64_t b = csn >> 8;
+      const int64_t len = int64_t(4 * (csn & 255)) * (3 * L + 1);
+      for (int64_t i = lane; i < len / 2; i += 32)
+        reinterpret_cast<double2*>(vals + b)[i] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+static size_t smem_bytes(bool) { return size_t(kSlotsPerTri) * TP * sizeof(double) + kPlanBytes; }
+
+template <bool NEED_J, bool N3>
+static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
+  static bool attr_set = false;
+  const size_t sm = smem_bytes(NEED_J);
+  if (!attr_set) {
+    fo_status st = cuda_status(cudaFuncSetAttribute(ka_patch_kernel<NEED_J, N3>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                               "cudaFuncSetAttribute");
+    if (st) return st;
+    attr_set = true;
+  }
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.contrib_ptr,
+              m->d_plan.cols, m->d_plan.pairs, m->d_plan.contrib};
+  ka_patch_kernel<NEED_J, N3><<<m->plan.n_patches, TP, sm, s>>>(
+      m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R, vals);
+  return cuda_status(cudaGetLastError(), "ka_patch_kernel launch");
+}
+
+fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s) {
+  const bool need_j = d_vals != nullptr;
+  // R is always produced by the kernel; use a scratch vector when the caller passes none
+  double* R = d_R;
+  if (!R) {
+    if (!m->d_scratch_R) {
+      fo_status st = cuda_status(cudaMalloc(&m->d_scratch_R, sizeof(double) * m->n_dof), "cudaMalloc");
+      if (st) return st;
+    }
+    R = m->d_scratch_R;
+  }
+  int launches = 0;
+  const int64_t nk_dof = 2 * (m->nA + m->nB) * (m->L + 1);
+  if (nk_dof < m->n_dof) {   // column-only (class C) DOFs: residual 0
+    fo_status st = cuda_status(cudaMemsetAsync(R + nk_dof, 0, sizeof(double) * (m->n_dof - nk_dof), s),
+                               "cudaMemsetAsync");
+    if (st) return st;
+  }
+  const int nz = int(m->plan.zero_cols.size());
+  if (nz > 0) {
+    const int blocks = int(std::min<int64_t>((int64_t(nz) * 32 + 255) / 256, 148 * 16));
+    zero_boundary_kernel<<<blocks, 256, 0, s>>>(m->d_col, m->d_plan.zero_cols, nz, m->L, R,
+                                                need_j ? d_vals : nullptr);
+    fo_status st = cuda_status(cudaGetLastError(), "zero_boundary_kernel launch");
+    if (st) return st;
+    ++launches;
+  }
+  const bool n3 = m->p.glen_n == 3.0;
+  fo_status st;
+  if (need_j)
+    st = n3 ? launch_patch<true, true>(m, d_U, R, d_vals, s) : launch_patch<true, false>(m, d_U, R, d_vals, s);
+  else
+    st = n3 ? launch_patch<false, true>(m, d_U, R, nullptr, s) : launch_patch<false, false>(m, d_U, R, nullptr, s);
+  if (st) return st;
+  m->last_launches = launches + 1;
+  return FO_OK;
+}
+
+}  // namespace fo

@@ -1,0 +1,165 @@
+// fo_plan.cpp -- host construction of the work decomposition of the
+// owner-computes assembly kernel (fo_owner.cu), DESIGN.md "KA-patch".
+//
+// A patch is a contiguous range of (Hilbert-ordered) local triangles, computed
+// by one CTA, one thread per triangle column.  For every column the patch
+// touches the plan stores a column record, and for every slot of the column's
+// coupling list a (column, slot) PAIR with its list of contributions: the
+// (patch-local triangle tl, local vertex j of the column, local vertex j' of
+// the slot's neighbour) whose element entries land in that slot.  Phase B of
+// the kernel gives one pair to one thread, which sums the 12 values (comp a,
+// level group g, comp b) of the slot for the current level.
+//
+// A column is INTERIOR to a patch when the patch holds its whole triangle
+// fan: its rows are written with plain stores (every slot, zeros included).
+// Otherwise it is a BOUNDARY column: its rows are zero-filled before the
+// kernel and every touching patch adds its partial sums with fp64 RED, for
+// the slots it contributes to only.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "fo_internal.h"
+
+namespace fo {
+
+namespace {
+template <class T>
+fo_status upload_vec(T** dst, const std::vector<T>& v) {
+  *dst = nullptr;
+  if (v.empty()) return FO_OK;
+  fo_status st = cuda_status(cudaMalloc(reinterpret_cast<void**>(dst), v.size() * sizeof(T)), "cudaMalloc");
+  if (st) return st;
+  return cuda_status(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+                     "cudaMemcpy H2D");
+}
+
+struct PatchBuild {
+  std::vector<PlanCol> cols;
+  std::vector<PlanPair> pairs;
+  std::vector<uint16_t> contrib;
+};
+
+// plan of the triangle range [t0, t1)
+void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int32_t t1,
+               PatchBuild& B, std::vector<char>& boundary) {
+  B.cols.clear();
+  B.pairs.clear();
+  B.contrib.clear();
+  std::vector<std::pair<int32_t, int32_t>> inc;   // (column, tl*4 + j)
+  for (int32_t t = t0; t < t1; ++t)
+    for (int j = 0; j < 3; ++j) inc.push_back({m->tri[size_t(3 * t + j)], (t - t0) * 4 + j});
+  std::sort(inc.begin(), inc.end());
+  size_t i = 0;
+  while (i < inc.size()) {
+    const int32_t c = inc[i].first;
+    size_t e = i;
+    while (e < inc.size() && inc[e].first == c) ++e;
+    const bool interior = int32_t(e - i) == fan[size_t(c)];
+    if (!interior) boundary[size_t(c)] = 1;
+    const int64_t nc = m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)];
+    const int32_t* lst = m->nbr.data() + m->nbr_ptr[size_t(c)];
+    const int32_t self = int32_t(std::lower_bound(lst, lst + nc, c) - lst);
+    std::vector<std::vector<uint16_t>> per_slot(static_cast<size_t>(nc));
+    for (size_t q = i; q < e; ++q) {
+      const int32_t tl = inc[q].second >> 2, j = inc[q].second & 3;
+      const TriRec& tr = m->trirec[size_t(t0 + tl)];
+      for (int j2 = 0; j2 < 3; ++j2)
+        per_slot[tr.slot[3 * j + j2]].push_back(uint16_t((tl << 4) | (j << 2) | j2));
+    }
+    PlanCol pc{};
+    pc.colstart = m->colstart[size_t(c)];
+    pc.c = c;
+    pc.info = int32_t(nc) | (interior ? 256 : 0) | (self << 9);
+    const int32_t ci = int32_t(B.cols.size());
+    for (int64_t s = 0; s < nc; ++s) {
+      const auto& l = per_slot[size_t(s)];
+      if (s == self) {
+        pc.self_off = uint16_t(B.contrib.size());
+        pc.self_cnt = uint16_t(l.size());
+      }
+      if (l.empty() && !interior) continue;   // boundary: only touched slots
+      PlanPair pp{};
+      pp.off = uint16_t(B.contrib.size());
+      pp.cnt = uint8_t(l.size());
+      pp.slot = uint8_t(s);
+      pp.col = uint16_t(ci);
+      B.pairs.push_back(pp);
+      B.contrib.insert(B.contrib.end(), l.begin(), l.end());
+    }
+    B.cols.push_back(pc);
+    i = e;
+  }
+}
+
+size_t plan_bytes(const PatchBuild& B) {
+  return B.cols.size() * sizeof(PlanCol) + B.pairs.size() * sizeof(PlanPair) +
+         ((B.contrib.size() * sizeof(uint16_t) + 15) / 16) * 16;
+}
+
+}  // namespace
+
+fo_status build_patch_plan(fo_mesh m) {
+  PatchPlan& P = m->plan;
+  P = PatchPlan();
+  const int64_t nt = m->n_tri;
+  const int64_t nk = m->nA + m->nB;     // columns with rows
+  if (nt == 0) return FO_OK;
+  std::vector<int32_t> fan(size_t(m->n_col), 0);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int j = 0; j < 3; ++j) fan[size_t(m->tri[size_t(3 * t + j)])]++;
+  std::vector<char> boundary(size_t(nk), 0);
+  P.t_begin.assign(1, 0);
+  P.col_ptr.assign(1, 0);
+  P.pair_ptr.assign(1, 0);
+  P.contrib_ptr.assign(1, 0);
+  PatchBuild B;
+  int64_t t0 = 0;
+  // equal-size ranges of at most kPatchTris triangles; a range whose plan
+  // exceeds the shared-memory budget is halved
+  const int64_t np0 = (nt + kPatchTris - 1) / kPatchTris;
+  std::vector<int64_t> bounds;
+  for (int64_t p = 0; p <= np0; ++p) bounds.push_back((p * nt) / np0);
+  for (size_t b = 0; b + 1 < bounds.size(); ++b) {
+    std::vector<std::pair<int64_t, int64_t>> todo{{bounds[b], bounds[b + 1]}};
+    while (!todo.empty()) {
+      auto [a0, a1] = todo.back();
+      todo.pop_back();
+      std::vector<char> bnd_tmp = boundary;
+      build_one(m, fan, int32_t(a0), int32_t(a1), B, bnd_tmp);
+      if (plan_bytes(B) > size_t(kPlanBytes) && a1 - a0 > 1) {
+        const int64_t mid = (a0 + a1) / 2;
+        todo.push_back({mid, a1});
+        todo.push_back({a0, mid});
+        continue;
+      }
+      boundary.swap(bnd_tmp);
+      t0 = a1;
+      P.t_begin.push_back(int32_t(a1));
+      P.cols.insert(P.cols.end(), B.cols.begin(), B.cols.end());
+      P.pairs.insert(P.pairs.end(), B.pairs.begin(), B.pairs.end());
+      P.contrib.insert(P.contrib.end(), B.contrib.begin(), B.contrib.end());
+      P.col_ptr.push_back(int32_t(P.cols.size()));
+      P.pair_ptr.push_back(int32_t(P.pairs.size()));
+      P.contrib_ptr.push_back(int64_t(P.contrib.size()));
+      P.max_plan_bytes = std::max<int64_t>(P.max_plan_bytes, int64_t(plan_bytes(B)));
+    }
+  }
+  (void)t0;
+  P.n_patches = int32_t(P.t_begin.size() - 1);
+  for (int64_t c = 0; c < nk; ++c)
+    if (boundary[size_t(c)]) P.zero_cols.push_back(int32_t(c));
+  fo_status st = upload_vec(&m->d_plan.t_begin, P.t_begin);
+  if (!st) st = upload_vec(&m->d_plan.col_ptr, P.col_ptr);
+  if (!st) st = upload_vec(&m->d_plan.pair_ptr, P.pair_ptr);
+  if (!st) st = upload_vec(&m->d_plan.contrib_ptr, P.contrib_ptr);
+  if (!st) st = upload_vec(&m->d_plan.cols, P.cols);
+  if (!st) st = upload_vec(&m->d_plan.pairs, P.pairs);
+  if (!st) st = upload_vec(&m->d_plan.contrib, P.contrib);
+  if (!st) st = upload_vec(&m->d_plan.zero_cols, P.zero_cols);
+  return st;
+}
+
+}  // namespace fo

@@ -18,12 +18,15 @@ print(f"mesh+graph {time.time()-t0:.1f}s nnz {g.nnz}", flush=True)
 U = torch.tensor(fp.U, device="cuda")
 R = torch.empty(mesh.n_dofs, dtype=torch.float64, device="cuda")
 V = torch.empty(g.nnz, dtype=torch.float64, device="cuda")
-for sc in (1, 0):
+import os
+modes = [int(x) for x in os.environ.get('FO_SCATTERS', '1,0').split(',')]
+whats = os.environ.get('FO_WHAT', 'residual,jacobian').split(',')
+for sc in modes:
     try:
         mesh.set_scatter(sc)
     except Exception as e:
         print("scatter", sc, e); continue
-    for what in ("residual", "jacobian"):
+    for what in whats:
         for _ in range(3):
             mesh.residual(U, R) if what == "residual" else mesh.jacobian(U, g, R, V)
         torch.cuda.synchronize()
