@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- FO-Stokes residual + Newton-Jacobian assembly throughput on B200.
+
+Metric (BASELINE.json): "FO-Stokes Jacobian+residual assembly Melem/s per GPU,
+% HBM roofline, 1-8 GPU".  One step = one Total Fill of PAPER.md P:388:
+[ghost import of U] -> fo_assemble_jacobian (R and J in one pass) ->
+[ghost-row sum], on a synthetic extruded Greenland-like mesh with 10 layers:
+  N = 1: config C3 (1-10 km graded footprint sized to the paper's 479,930
+         triangles), 4.8 M wedges;
+  N > 1: config C4, the C3 recipe refined to N x 479,930 triangles, footprint
+         partitioned into N Hilbert-contiguous parts (weak scaling), NCCL halo.
+value = all wedges of all ranks per second / 1e6 (Melem/s, whole job), timed
+with CUDA events around every step (L2 flushed between steps, outside the
+events), max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference runs the CPU oracle (oracle/, the serial C++ FE assembly the
+CUDA path is validated against) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FO-Stokes Jacobian+residual assembly Melem/s per GPU, % HBM roofline, 1-8 GPU"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x max clock
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scatter", type=int, default=0, help="0 owner-computes (default), 1 atomic")
+    ap.add_argument("--cpu-sample-tris", type=int, default=40000)
+    ap.add_argument("--ref-sample-tris", type=int, default=3000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload(n_gpus: int):
+    from paper_2204_04321_b200 import meshgen as mg
+    if n_gpus == 1:
+        return mg.greenland_like_1_10(), "C3"
+    return mg.greenland_like_1_10(scale=float(n_gpus)), f"C4x{n_gpus}"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.2)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(n_elem, nnz, n_nodes, n_cols, n_tri, has_A):
+    """J values written once, R written, U read, column
+    records (x, y, s, H, beta), triangle connectivity, per-wedge A if a field."""
+    return 8 * nnz + 16 * n_nodes + 16 * n_nodes + 40 * n_cols + 12 * n_tri + (8 * n_elem if has_A else 0)
+
+
+def ncu_summary(config_name):
+    """dram traffic / fp64 counts of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d if d.get("config") == config_name else None
+
+
+def cpu_baseline_oracle(fp, n_tri_sample):
+    """The oracle (serial C++, Dual<12> AD Jacobian) on the first n_tri_sample
+    Hilbert-contiguous triangles of the same workload, on 1 host core."""
+    from oracle import oracle as ora
+    from paper_2204_04321_b200 import meshgen as mg
+    ora.build()
+    sub = mg.sub_footprint(fp, 0, min(n_tri_sample, fp.n_tri))
+    o = ora.Oracle(sub)
+    o.graph()                                  # brute-force graph: setup, untimed
+    t0 = time.perf_counter()
+    o.jacobian(sub.U)
+    dt = time.perf_counter() - t0
+    return {"value": sub.n_elem / dt / 1e6, "unit": "Melem/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sub.n_tri} triangles x {sub.n_layers} layers = {sub.n_elem} wedges of "
+                      f"{fp.name}: oracle residual + Dual<12> AD Jacobian (one call, {dt:.2f} s, serial, -O2)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    fp, name = workload(args.gpus)
+    from oracle import oracle as ora
+    from paper_2204_04321_b200 import meshgen as mg
+    ora.build()
+    sub = mg.sub_footprint(fp, 0, min(args.ref_sample_tris, fp.n_tri))
+    o = ora.Oracle(sub)
+    o.graph()
+    for _ in range(args.warmup):
+        o.jacobian(sub.U)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.jacobian(sub.U)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = sub.n_elem * args.steps / tot / 1e6
+    sample = (f"{sub.n_elem} wedges per step (first {sub.n_tri} triangles of {fp.name}), "
+              f"serial oracle R + Dual<12> AD Jacobian")
+    line = {"metric": METRIC, "value": value, "unit": "Melem/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{name}: {fp.name}, sample of {sub.n_tri} triangles x {sub.n_layers} layers",
+                       "n_elem": sub.n_elem},
+            "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2204_04321_b200 import _build, fo
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+
+    fp, cfg_name = workload(world)
+    L = fp.n_layers
+    if world == 1:
+        mesh = fo.Mesh.from_footprint(fp, device=local)
+        U_local = fp.U
+        halo = None
+    else:
+        part = fo.partition(fp.n_tri, world)
+        mesh = fo.Mesh.from_footprint(fp, device=local, part=part, my_part=rank, n_parts=world)
+        glob = mesh.columns()[0]
+        U_local = fp.U.reshape(fp.n_vert, L + 1, 2)[glob].reshape(-1)
+        obj = [fo.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        halo = fo.Halo(mesh, obj[0], rank, world)
+    mesh.set_scatter(args.scatter)
+    graph = mesh.graph()
+    glob, nA, nB, nC = mesh.columns()
+    n_cols = nA + nB
+    n_tri_local = mesh.n_elems // L
+    U = torch.tensor(U_local, dtype=torch.float64, device=dev)
+    R = torch.empty(mesh.n_dofs, dtype=torch.float64, device=dev)
+    V = torch.empty(graph.nnz, dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)   # 512 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if halo is not None:
+            halo.import_(U)
+        mesh.jacobian(U, graph, R, V)
+        if halo is not None:
+            halo.sum(R, V)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = mesh.last_launch_count()
+    if halo is not None:
+        nn, _, _ = halo.info()
+        launches_per_step += 4 * nn   # gather + scatter-add kernels of the halo (upper bound)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    mesh.kernel_timing(True)
+    evs = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.zero_()                        # evict inputs from L2 (outside the timed span)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    mesh.kernel_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    kern_ms, kern_n = mesh.kernel_time_ms()
+    tot_ms = sum(step_ms)
+    elems = mesh.n_elems
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        e = torch.tensor([elems], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        elems = int(e.item())
+    value = elems * args.steps / (tot_ms / 1e3) / 1e6
+
+    # roofline of the dominant kernel (ka_patch_kernel), this rank
+    peak, peak_src = measured_peaks()
+    has_A = fp.A_elem is not None
+    alg = algorithmic_bytes(mesh.n_elems, graph.nnz, mesh.n_nodes, n_cols, n_tri_local, has_A)
+    kavg = kern_ms / max(kern_n, 1)
+    achieved = alg / (kavg / 1e3) / 1e9
+    prof = ncu_summary(cfg_name)
+    traffic = None
+    fp64 = None
+    if prof:
+        traffic = prof.get("dram_bytes_per_launch")
+        fpw = prof.get("fp64_flop_per_wedge")
+        if fpw:
+            tfl = fpw * mesh.n_elems / (kavg / 1e3) / 1e12
+            fp64 = {"achieved": tfl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": tfl / FP64_PEAK_TFLOPS,
+                    "flop_per_wedge": fpw, "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz",
+                    "flop_source": prof.get("source")}
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "ka_patch_kernel" if args.scatter == 0 else "assemble_atomic_kernel",
+            "kernel_ms": kavg, "kernel_share_of_step": kern_ms / max(sum(step_ms), 1e-12),
+            "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+            "bytes_formula": "8 nnz + 32 N_nodes + 40 N_cols + 12 N_tri (SURVEY.md 8(d) d3)"}
+    if fp64:
+        roof["fp64"] = fp64
+
+    # end to end through the C ABI with host buffers (pinned)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        Uh = torch.tensor(U_local, dtype=torch.float64).pin_memory()
+        Rh = torch.empty(mesh.n_dofs, dtype=torch.float64).pin_memory()
+        Vh = torch.empty(graph.nnz, dtype=torch.float64).pin_memory()
+        mesh.jacobian_host(Uh, Rh, Vh, graph)          # warm-up (staging allocation)
+        tms = []
+        for _ in range(args.e2e_steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            mesh.jacobian_host(Uh, Rh, Vh, graph)
+            b.record(stream)
+            b.synchronize()
+            tms.append(a.elapsed_time(b))
+        e2e = {"value": mesh.n_elems * len(tms) / (sum(tms) / 1e3) / 1e6, "unit": "Melem/s",
+               "h2d_bytes_per_step": 8 * mesh.n_dofs, "d2h_bytes_per_step": 8 * (mesh.n_dofs + graph.nnz),
+               "api": "fo_assemble_jacobian_host (pinned host U in, R and CSR values out)"}
+    elif world > 1 and args.e2e_steps > 0:
+        n_owned = mesh.n_owned_dofs
+        owned_vals = int(graph.row_ptr_host()[n_owned])
+        Uh = torch.tensor(U_local[:n_owned], dtype=torch.float64).pin_memory()
+        Rh = torch.empty(n_owned, dtype=torch.float64).pin_memory()
+        Vh = torch.empty(owned_vals, dtype=torch.float64).pin_memory()
+        tms = []
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            U[:n_owned].copy_(Uh, non_blocking=True)
+            step()
+            Rh.copy_(R[:n_owned], non_blocking=True)
+            Vh.copy_(V[:owned_vals], non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            tms.append(a.elapsed_time(b))
+        t = torch.tensor([sum(tms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": elems * len(tms) / (float(t.item()) / 1e3) / 1e6, "unit": "Melem/s",
+               "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * (n_owned + owned_vals),
+               "api": "torch H2D of owned U -> fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum -> D2H owned rows"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_oracle(fp, args.cpu_sample_tris)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Melem/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Greenland-like footprint, SIA velocity; SURVEY.md 8(d) d1)",
+            "config": {"workload": f"{cfg_name}: {fp.name}, {fp.n_tri} triangles x {L} layers = "
+                                   f"{fp.n_elem} wedges, {world} part(s)",
+                       "wedges_per_gpu": mesh.n_elems, "nnz_per_gpu": graph.nnz, "n_dofs_per_gpu": mesh.n_dofs,
+                       "parallelism": f"footprint partition x{world}" + (", NCCL halo" if world > 1 else ""),
+                       "scatter": "owner-computes" if args.scatter == 0 else "atomic",
+                       "l2": "1.7 GB of CSR values written per step (> 126 MB L2) and a 512 MB buffer "
+                             "written between timed steps"},
+            "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk, "cpu_baseline": cpu,
+            "per_step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,13 @@ FO_API fo_status fo_set_scatter(fo_mesh m, fo_scatter s);
 /* Kernel launches the last assembly call enqueued (for bench accounting). */
 FO_API fo_status fo_last_launch_count(fo_mesh m, int32_t* n);
 
+/* Kernel timing (bench): while enabled, every assembly call records a pair of
+ * CUDA events around its main assembly kernel on the caller's stream.
+ * fo_kernel_time_ms synchronises the recorded events, returns the summed
+ * elapsed milliseconds and the number of timed launches, and clears them. */
+FO_API fo_status fo_kernel_timing(fo_mesh m, int32_t enable);
+FO_API fo_status fo_kernel_time_ms(fo_mesh m, double* total_ms, int32_t* n_launches);
+
 /* ---- multi-GPU halo (P:175 Import, P:185 Export) ----
  * nccl_unique_id: 128-byte ncclUniqueId, identical on all ranks (rank 0
  * creates it with fo_nccl_unique_id and the harness broadcasts it).

@@ -546,6 +546,31 @@ fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   return FO_OK;
 }
 
+fo_status fo_kernel_timing(fo_mesh m, int32_t enable) {
+  if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  m->timing = enable != 0;
+  return FO_OK;
+}
+
+fo_status fo_kernel_time_ms(fo_mesh m, double* total_ms, int32_t* n_launches) {
+  if (!m || !total_ms) return fail(FO_EINVAL, "NULL argument");
+  double tot = 0.0;
+  fo_status st = FO_OK;
+  for (auto& pr : m->timed) {
+    cudaEvent_t a = static_cast<cudaEvent_t>(pr.first), b = static_cast<cudaEvent_t>(pr.second);
+    float ms = 0.0f;
+    if (!st) st = cuda_status(cudaEventSynchronize(b), "cudaEventSynchronize");
+    if (!st) st = cuda_status(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+    tot += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  if (n_launches) *n_launches = int32_t(m->timed.size());
+  m->timed.clear();
+  *total_ms = tot;
+  return st;
+}
+
 fo_status fo_last_launch_count(fo_mesh m, int32_t* n) {
   if (!m || !n) return fail(FO_EINVAL, "NULL argument");
   *n = m->last_launches;
@@ -571,6 +596,10 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_stage_R);
   cudaFree(m->d_stage_vals);
   cudaFree(m->d_scratch_R);
+  for (auto& pr : m->timed) {
+    cudaEventDestroy(static_cast<cudaEvent_t>(pr.first));
+    cudaEventDestroy(static_cast<cudaEvent_t>(pr.second));
+  }
   delete m;
 }
 

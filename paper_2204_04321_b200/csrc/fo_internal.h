@@ -110,6 +110,8 @@ struct fo_mesh_s {
   fo::DevPatch d_plan;
   fo_scatter scatter = FO_SCATTER_OWNER;
   int32_t last_launches = 0;
+  bool timing = false;
+  std::vector<std::pair<void*, void*>> timed;   // (start, stop) cudaEvent_t pairs
   // host-API staging
   double* d_stage_U = nullptr;
   double* d_stage_R = nullptr;

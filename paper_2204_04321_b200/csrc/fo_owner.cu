@@ -316,8 +316,18 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
   }
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.contrib_ptr,
               m->d_plan.cols, m->d_plan.pairs, m->d_plan.contrib};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (m->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
   ka_patch_kernel<NEED_J, N3><<<m->plan.n_patches, TP, sm, s>>>(
       m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R, vals);
+  if (m->timing) {
+    cudaEventRecord(e1, s);
+    m->timed.push_back({e0, e1});
+  }
   return cuda_status(cudaGetLastError(), "ka_patch_kernel launch");
 }
 

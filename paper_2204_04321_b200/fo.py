@@ -60,6 +60,8 @@ _SIGS = {
     "fo_assemble_jacobian_host": [P, P, P, P, P, P],
     "fo_set_scatter": [P, C.c_int],
     "fo_last_launch_count": [P, P],
+    "fo_kernel_timing": [P, I32],
+    "fo_kernel_time_ms": [P, P, P],
     "fo_nccl_unique_id": [P],
     "fo_halo_create": [P, P, P, I32, I32, P],
     "fo_halo_import": [P, P, P],
@@ -187,6 +189,46 @@ def halo_plan_host(n_vert, tri, n_layers, part, n_parts, my_part):
     return out
 
 
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    check(lib().fo_nccl_unique_id(buf), "fo_nccl_unique_id")
+    return bytes(buf)
+
+
+class Halo:
+    """NCCL ghost import / ghost-row sum of a partitioned mesh (collective)."""
+
+    def __init__(self, mesh: "Mesh", uid: bytes, rank: int, n_ranks: int):
+        self.mesh = mesh
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib().fo_halo_create(mesh.handle, mesh.graph().handle, buf, rank, n_ranks, C.byref(h)),
+              "fo_halo_create")
+        self.handle = h
+
+    def info(self):
+        nn, rr, rv = C.c_int32(), C.c_int64(), C.c_int64()
+        check(lib().fo_halo_info(self.handle, C.byref(nn), C.byref(rr), C.byref(rv)), "fo_halo_info")
+        return nn.value, rr.value, rv.value
+
+    def import_(self, U, stream=None):
+        check(lib().fo_halo_import(self.handle, _ptr(U), _stream_ptr(stream)), "fo_halo_import")
+
+    def sum(self, R=None, vals=None, stream=None):
+        check(lib().fo_halo_sum(self.handle, _ptr(R), _ptr(vals), _stream_ptr(stream)), "fo_halo_sum")
+
+    def close(self):
+        if self.handle:
+            lib().fo_halo_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Graph:
     def __init__(self, mesh: "Mesh"):
         self.mesh = mesh
@@ -196,6 +238,11 @@ class Graph:
         n_rows, nnz = C.c_int64(), C.c_int64()
         check(lib().fo_graph_info(h, C.byref(n_rows), C.byref(nnz)), "fo_graph_info")
         self.n_rows, self.nnz = n_rows.value, nnz.value
+
+    def row_ptr_host(self):
+        row_ptr = np.zeros(self.n_rows + 1, dtype=np.int64)
+        check(lib().fo_graph_to_host(self.handle, _ptr(row_ptr), None), "fo_graph_to_host")
+        return row_ptr
 
     def to_host(self):
         row_ptr = np.zeros(self.n_rows + 1, dtype=np.int64)
@@ -281,6 +328,15 @@ class Mesh:
 
     def set_scatter(self, mode: int):
         check(lib().fo_set_scatter(self.handle, int(mode)), "fo_set_scatter")
+
+    def kernel_timing(self, on: bool):
+        check(lib().fo_kernel_timing(self.handle, 1 if on else 0), "fo_kernel_timing")
+
+    def kernel_time_ms(self):
+        """(summed ms, launches) of the main kernel since the last call."""
+        ms, n = C.c_double(), C.c_int32()
+        check(lib().fo_kernel_time_ms(self.handle, C.byref(ms), C.byref(n)), "fo_kernel_time_ms")
+        return ms.value, n.value
 
     def last_launch_count(self) -> int:
         n = C.c_int32()

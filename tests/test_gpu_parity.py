@@ -199,3 +199,52 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod):
                 seg_o = ov[orp[r_o]:orp[r_o + 1]]
                 assert seg_g.size == seg_o.size
                 assert np.abs(seg_g - seg_o).max() <= J_TOL * np.abs(seg_o).max()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P):
+    """local meshes of a P-way footprint partition (fo_mesh_create_part) on one
+    GPU, ghost-row partial sums added into the owners with the library's halo
+    plan (the data movement fo_halo_sum does over NCCL): owned rows equal the
+    single-domain assembly; ghost import fills the ghost U slices."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like(40.0, n_layers=5)
+    L = fp.n_layers
+    part = fo.partition(fp.n_tri, P)
+    full = fo.Mesh.from_footprint(fp)
+    Rf, Vf = full.jacobian(torch.tensor(fp.U, device="cuda"))
+    grp, gcol = full.graph().to_host()
+    Rf, Vf = Rf.cpu().numpy(), Vf.cpu().numpy()
+    meshes, outs = [], []
+    for p in range(P):
+        m = fo.Mesh.from_footprint(fp, part=part, my_part=p, n_parts=P)
+        glob, nA, nB, nC = m.columns()
+        Ul = fp.U.reshape(fp.n_vert, L + 1, 2)[glob].reshape(-1)
+        R, V = m.jacobian(torch.tensor(Ul, device="cuda"))
+        meshes.append((m, glob, nA))
+        outs.append([R, V])
+    torch.cuda.synchronize()
+    plans = [fo.halo_plan_host(fp.n_vert, fp.tri, L, part, P, p) for p in range(P)]
+    for p in range(P):
+        for q, (sr, dr, sv, dv) in plans[p].items():
+            Rq, Vq = outs[q]
+            Rq.index_add_(0, torch.tensor(dr, device="cuda"), outs[p][0][torch.tensor(sr, device="cuda")])
+            Vq.index_add_(0, torch.tensor(dv, device="cuda"), outs[p][1][torch.tensor(sv, device="cuda")])
+    torch.cuda.synchronize()
+    for p in range(P):
+        m, glob, nA = meshes[p]
+        rp, col = m.graph().to_host()
+        L1 = L + 1
+        g = (np.stack([2 * (glob[:, None] * L1 + np.arange(L1)), 2 * (glob[:, None] * L1 + np.arange(L1)) + 1],
+                      axis=2)).reshape(-1)
+        R = outs[p][0].cpu().numpy()
+        V = outs[p][1].cpu().numpy()
+        n_owned = m.n_owned_dofs
+        assert np.abs(R[:n_owned] - Rf[g[:n_owned]]).max() <= 1e-12 * np.abs(Rf).max()
+        for r in range(0, n_owned, 3):
+            gr = g[r]
+            seg = Vf[grp[gr]:grp[gr + 1]]
+            loc = V[rp[r]:rp[r + 1]]
+            order = np.argsort(g[col[rp[r]:rp[r + 1]]])
+            assert np.abs(loc[order] - seg).max() <= 1e-11 * np.abs(seg).max()
