@@ -176,27 +176,6 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       }
     }
   }
-  // ---- viscous residual R_{a,(j,l)} = sum_q c_q (f_l P^a_j + sigma_l r_j Q^a)
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    double ub = 0.0, vb = 0.0, ut = 0.0, vt = 0.0;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const int a = q >> 1;
-      const double f0 = (q & 1) ? 0.5 - 0.5 * kZeta : 0.5 + 0.5 * kZeta;
-      const double crj = cq[q] * ((j == a) ? kTwoThirds : kSixth) * rho[a];
-      const double cpu = cq[q] * fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
-      const double cpv = cq[q] * fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
-      ub = fma(f0, cpu, fma(-crj, Qu(q), ub));
-      vb = fma(f0, cpv, fma(-crj, Qv(q), vb));
-      ut = fma(1.0 - f0, cpu, fma(crj, Qu(q), ut));
-      vt = fma(1.0 - f0, cpv, fma(crj, Qv(q), vt));
-    }
-    sink.r_bot_add(2 * j, ub);
-    sink.r_bot_add(2 * j + 1, vb);
-    sink.r_top_add(2 * j, ut);
-    sink.r_top_add(2 * j + 1, vt);
-  }
   // ---- frozen-viscosity part in closed form from the six c_q
   double F[3];                        // F_00, F_01, F_11 = sum c f_l f_l'
   double T2x[2][3], T2y[2][3];        // sum c f_l z_x r_j, sum c f_l z_y r_j
@@ -294,31 +273,30 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   // section (an IEEE-exact no-op that orders the blocks), so one accumulator
   // set is live at a time.
   double gate = 0.0;
-  if (w.go) {   // frozen-viscosity (top, top): first writes of the held block
+  if (w.go) {
+    // frozen-viscosity part, emitted node pair by node pair (j <= j2) so the
+    // G / AA combinations of a pair are shared by its entries of all three
+    // level blocks: (top, top) -> held (first write), (bottom, top) -> O
+    // (first write), (bottom, bottom) -> D (added)
 #pragma unroll
-    for (int p = 0; p < 6; ++p)
+    for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int p2 = p; p2 < 6; ++p2) {
-        const double v = hpart(p & 1, p >> 1, 1, p2 & 1, p2 >> 1, 1);
-        sink.top(pk6(p, p2), v);
-        gate = v;
+      for (int j2 = j; j2 < 3; ++j2) {
+#pragma unroll
+        for (int ca = 0; ca < 2; ++ca)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) {
+            const int p = 2 * j + ca, p2 = 2 * j2 + cb;
+            if (p <= p2) {
+              sink.top(pk6(p, p2), hpart(ca, j, 1, cb, j2, 1));
+              sink.bot_add(p, p2, hpart(ca, j, 0, cb, j2, 0));
+            }
+            const double v = hpart(ca, j, 0, cb, j2, 1);
+            sink.off(p, p2, v);
+            gate = v;
+            if (j != j2) sink.off(p2, p, hpart(cb, j2, 0, ca, j, 1));
+          }
       }
-  }
-  if (w.go) {   // frozen-viscosity (bottom, top): first writes
-#pragma unroll
-    for (int p = 0; p < 6; ++p)
-#pragma unroll
-      for (int p2 = 0; p2 < 6; ++p2) {
-        const double v = hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 1);
-        sink.off(p, p2, v);
-        gate = v;
-      }
-  }
-  if (w.go) {   // frozen-viscosity (bottom, bottom)
-#pragma unroll
-    for (int p = 0; p < 6; ++p)
-#pragma unroll
-      for (int p2 = p; p2 < 6; ++p2) sink.bot_add(p, p2, hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 0));
   }
   if (w.go) {   // rank-1 (bottom, top)
     double acc[36];
@@ -353,10 +331,12 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       for (int p2 = 0; p2 < 6; ++p2) sink.off_add(p, p2, acc[6 * p + p2]);
     gate = acc[35];
   }
-  if (w.go) {   // rank-1 (bottom, bottom)
-    double acc[21];
+  if (w.go) {   // rank-1 (bottom, bottom) and the bottom viscous residual
+    double acc[21], res[6];
 #pragma unroll
     for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) res[i] = 0.0;
 #pragma unroll 1
     for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
       const int a = q >> 1;
@@ -371,8 +351,12 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         g[2 * j] = fma(f0, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), -rj * Qu(q));
         g[2 * j + 1] = fma(f0, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), -rj * Qv(q));
       }
+      const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
 #pragma unroll
-      for (int p = 0; p < 6; ++p) dg[p] = dd * g[p];
+      for (int p = 0; p < 6; ++p) {
+        dg[p] = dd * g[p];
+        res[p] = fma(cc, g[p], res[p]);   // R_{a,(j,0)} += c_q g
+      }
 #pragma unroll
       for (int p = 0; p < 6; ++p)
 #pragma unroll
@@ -382,12 +366,16 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     for (int p = 0; p < 6; ++p)
 #pragma unroll
       for (int p2 = p; p2 < 6; ++p2) sink.bot_add(p, p2, acc[pk6(p, p2)]);
+#pragma unroll
+    for (int p = 0; p < 6; ++p) sink.r_bot_add(p, res[p]);
     gate = acc[20];
   }
-  if (w.go) {   // rank-1 (top, top), added to the held block
-    double acc[21];
+  if (w.go) {   // rank-1 (top, top), added to the held block; the top viscous residual
+    double acc[21], res[6];
 #pragma unroll
     for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) res[i] = 0.0;
 #pragma unroll 1
     for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
       const int a = q >> 1;
@@ -402,8 +390,12 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         g[2 * j] = fma(f1, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), rj * Qu(q));
         g[2 * j + 1] = fma(f1, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), rj * Qv(q));
       }
+      const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
 #pragma unroll
-      for (int p = 0; p < 6; ++p) dg[p] = dd * g[p];
+      for (int p = 0; p < 6; ++p) {
+        dg[p] = dd * g[p];
+        res[p] = fma(cc, g[p], res[p]);   // R_{a,(j,1)} += c_q g
+      }
 #pragma unroll
       for (int p = 0; p < 6; ++p)
 #pragma unroll
@@ -411,6 +403,8 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     }
 #pragma unroll
     for (int i = 0; i < 21; ++i) sink.top_add(i, acc[i]);
+#pragma unroll
+    for (int p = 0; p < 6; ++p) sink.r_top_add(p, res[p]);
   }
 #undef dq
 #undef E1x

@@ -29,9 +29,15 @@ struct alignas(8) TriRec {
 
 // Triangles per patch of the owner-computes kernel (one thread per triangle
 // column, 105 fp64 of shared memory per triangle).
-constexpr int kPatchTris = 240;
+constexpr int kPatchTris = 120;
+// CTAs resident per SM (2: one CTA's gather phase overlaps the other's
+// element phase)
+constexpr int kPatchCtasPerSm = 2;
+// row stride (doubles) of the [entry][triangle] shared-memory arrays: odd, so
+// entries of one triangle fall in different banks
+constexpr int kPatchStride = kPatchTris + 1;
 // shared-memory budget of one patch's plan (columns, pairs, contributions)
-constexpr int kPlanBytes = 232448 - 105 * kPatchTris * 8 - 256;
+constexpr int kPlanBytes = (233472 - 1024 * kPatchCtasPerSm) / kPatchCtasPerSm - 105 * kPatchStride * 8 - 64;
 
 // plan records (fo_plan.cpp); copied to shared memory by the kernel
 struct PlanCol {            // 24 bytes
@@ -60,7 +66,7 @@ struct PatchPlan {
   std::vector<int64_t> contrib_ptr;  // [n_patches+1]
   std::vector<PlanCol> cols;
   std::vector<PlanPair> pairs;
-  std::vector<uint16_t> contrib;     // tl << 4 | j << 2 | j'
+  std::vector<uint32_t> contrib;     // encoded contribution (fo_plan.cpp contrib_code)
   std::vector<int32_t> zero_cols;    // boundary columns (zero-filled before the kernel)
 };
 
@@ -71,7 +77,7 @@ struct DevPatch {
   int64_t* contrib_ptr = nullptr;
   PlanCol* cols = nullptr;
   PlanPair* pairs = nullptr;
-  uint16_t* contrib = nullptr;
+  uint32_t* contrib = nullptr;
   int32_t* zero_cols = nullptr;
 };
 

@@ -36,10 +36,10 @@ struct PlanView {
   const int64_t* __restrict__ contrib_ptr;
   const PlanCol* __restrict__ cols;
   const PlanPair* __restrict__ pairs;
-  const uint16_t* __restrict__ contrib;
+  const uint32_t* __restrict__ contrib;
 };
 
-constexpr int TP = kPatchTris;
+constexpr int TP = kPatchStride;   // SoA row stride (threads per CTA: kPatchTris)
 constexpr int kD = 27;   // level-k diagonal block (21, 2x2-block layout) + 6 residual
 constexpr int kO = 36;   // 6x6 bottom-top block of wedge k
 constexpr int kC = 42;   // compact per-point scratch (7 x 6 quadrature points)
@@ -61,7 +61,7 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 struct SmemPlan {
   const PlanCol* cols;
   const PlanPair* pairs;
-  const uint16_t* contrib;
+  const uint32_t* contrib;
   int ncols, npairs;
 };
 
@@ -79,79 +79,87 @@ __device__ __forceinline__ void put2(double* dst, double x, double y, bool inter
 // gathers: level-kk rows, column level kk (from D) and kk+1 (from O); level
 // kk+1 rows, column level kk (from O transposed).  The level-kk rows' column
 // level kk-1 part was written by the previous call (partial rows, merged in
-// L2).  The self slot also gathers the residual of node (c, kk).
-template <bool NEED_J>
-__device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const double* D,
-                                        const double* O, double* __restrict__ R,
-                                        double* __restrict__ vals) {
-  const bool has_up = kk < L;
+// L2).  Pairs are ordered by contribution count in the plan, so the lanes of a
+// warp run loops of (nearly) equal length.  Then one thread per column
+// gathers the residual of node (c, kk) from the self slot.
+template <bool UP>
+__device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
+                                          const double* O, double* __restrict__ vals) {
   const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // groups of level-kk rows
   const int m1 = (kk + 1 == L) ? 2 : 3;                   // groups of level-kk+1 rows
   const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
   const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk row slot
-  if (!NEED_J) {
-    for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
-      const PlanCol& pc = sp.cols[ci];
-      double r0 = 0.0, r1 = 0.0;
-      for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; ++e) {
-        const int cb = sp.contrib[e];
-        const int tl = cb >> 4, j = (cb >> 2) & 3;
-        r0 += D[(21 + 2 * j) * TP + tl];
-        r1 += D[(22 + 2 * j) * TP + tl];
-      }
-      put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
-    }
-    return;
-  }
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
     const PlanCol& pc = sp.cols[pp.col];
-    const int nc = pc.info & 255;
-    const bool interior = (pc.info >> 8) & 1;
-    const bool is_self = pp.slot == ((pc.info >> 9) & 255);
-    double dg[2][2], up[2][2], nx[2][2], rr[2] = {0.0, 0.0};
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) dg[a][b] = up[a][b] = nx[a][b] = 0.0;
-    for (int e = pp.off; e < pp.off + pp.cnt; ++e) {
-      const int cb = sp.contrib[e];
-      const int tl = cb >> 4, j = (cb >> 2) & 3, j2 = cb & 3;
-      int dbase, sa, sb;
-      if (j == j2) { dbase = 12 + 3 * j; sa = 1; sb = 1; }
-      else { dbase = 4 * (j + j2 - 1); sa = j < j2 ? 2 : 1; sb = j < j2 ? 1 : 2; }
-      const double* Dt = D + tl;
-      const double* Ot = O + tl;
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          dg[a][b] += Dt[(dbase + sa * a + sb * b) * TP];
-          if (has_up) {
-            up[a][b] += Ot[(6 * (2 * j + a) + 2 * j2 + b) * TP];
-            nx[a][b] += Ot[(6 * (2 * j2 + b) + 2 * j + a) * TP];
-          }
-        }
-      if (is_self) {
-        rr[0] += Dt[(21 + 2 * j) * TP];
-        rr[1] += Dt[(22 + 2 * j) * TP];
+    double dg00 = 0.0, dg01 = 0.0, dg10 = 0.0, dg11 = 0.0;
+    double up00 = 0.0, up01 = 0.0, up10 = 0.0, up11 = 0.0;
+    double nx00 = 0.0, nx01 = 0.0, nx10 = 0.0, nx11 = 0.0;
+    const uint32_t* cp = sp.contrib + pp.off;
+    for (int e = 0; e < pp.cnt; ++e) {
+      const uint32_t cb = cp[e];
+      const int tl = int(cb & 255);
+      const int pat = int((cb >> 13) & 3);
+      const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
+      const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
+      dg00 += Dt[0];
+      dg01 += Dt[sb];
+      dg10 += Dt[sa];
+      dg11 += Dt[sa + sb];
+      if (UP) {
+        const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
+        const double* On = O + int((cb >> 20) & 31) * TP + tl;
+        up00 += Ou[0];
+        up01 += Ou[TP];
+        up10 += Ou[6 * TP];
+        up11 += Ou[7 * TP];
+        nx00 += On[0];
+        nx01 += On[6 * TP];
+        nx10 += On[TP];
+        nx11 += On[7 * TP];
       }
     }
-    if (!interior && pp.cnt == 0) continue;
+    const int nc = pc.info & 255;
+    const bool interior = (pc.info >> 8) & 1;
     const int64_t seg0 = pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      double* d0 = vals + seg0 + int64_t(a) * (2 * nc * m0);
-      put2(d0, dg[a][0], dg[a][1], interior);
-      if (has_up) put2(d0 + 2, up[a][0], up[a][1], interior);
+    double* d0 = vals + seg0;
+    double* d1 = d0 + 2 * nc * m0;
+    put2(d0, dg00, dg01, interior);
+    put2(d1, dg10, dg11, interior);
+    if (UP) {
+      put2(d0 + 2, up00, up01, interior);
+      put2(d1 + 2, up10, up11, interior);
+      double* e0 = vals + pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
+      put2(e0, nx00, nx01, interior);
+      put2(e0 + 2 * nc * m1, nx10, nx11, interior);
     }
-    if (has_up) {
-      const int64_t seg1 = pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
-#pragma unroll
-      for (int a = 0; a < 2; ++a) put2(vals + seg1 + int64_t(a) * (2 * nc * m1), nx[a][0], nx[a][1], interior);
-    }
-    if (is_self) put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), rr[0], rr[1], interior);
   }
+}
+
+__device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, const double* D,
+                                          double* __restrict__ R) {
+  for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
+    const PlanCol& pc = sp.cols[ci];
+    double r0 = 0.0, r1 = 0.0;
+    for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; ++e) {
+      const uint32_t cb = sp.contrib[e];
+      const double* Dr = D + (21 + 2 * int((cb >> 25) & 3)) * TP + int(cb & 255);
+      r0 += Dr[0];
+      r1 += Dr[TP];
+    }
+    put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
+  }
+}
+
+template <bool NEED_J>
+__device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const double* D,
+                                        const double* O, double* __restrict__ R,
+                                        double* __restrict__ vals) {
+  if (NEED_J) {
+    if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals);
+    else phase_b_j<false>(sp, kk, L, D, O, vals);
+  }
+  phase_b_r(sp, kk, L, D, R);
 }
 
 // Sink of wedge_element_v4: bottom parts added to D and O in shared memory,
@@ -207,7 +215,7 @@ struct SmemCmp {
 };
 
 template <bool NEED_J, bool N3>
-__global__ void __launch_bounds__(TP, 1)
+__global__ void __launch_bounds__(kPatchTris, kPatchCtasPerSm)
 ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
                 const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
                 PlanView pv, const double* __restrict__ U, double* __restrict__ R,
@@ -227,7 +235,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     char* base = reinterpret_cast<char*>(smem + kSlotsPerTri * TP);
     PlanCol* cs = reinterpret_cast<PlanCol*>(base);
     PlanPair* ps = reinterpret_cast<PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
-    uint16_t* es = reinterpret_cast<uint16_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
+    uint32_t* es = reinterpret_cast<uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
     for (int i = threadIdx.x; i < (c1 - c0) * int(sizeof(PlanCol) / 8); i += blockDim.x)
       reinterpret_cast<int2*>(cs)[i] = __ldg(reinterpret_cast<const int2*>(pv.cols + c0) + i);
     for (int i = threadIdx.x; i < q1 - q0; i += blockDim.x)
@@ -322,7 +330,7 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  ka_patch_kernel<NEED_J, N3><<<m->plan.n_patches, TP, sm, s>>>(
+  ka_patch_kernel<NEED_J, N3><<<m->plan.n_patches, kPatchTris, sm, s>>>(
       m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R, vals);
   if (m->timing) {
     cudaEventRecord(e1, s);

@@ -39,8 +39,25 @@ fo_status upload_vec(T** dst, const std::vector<T>& v) {
 struct PatchBuild {
   std::vector<PlanCol> cols;
   std::vector<PlanPair> pairs;
-  std::vector<uint16_t> contrib;
+  std::vector<uint32_t> contrib;
 };
+
+// Contribution of wedge-triangle tl (local vertex j = the row column, j2 = the
+// slot's column) encoded with the shared-memory offsets phase B needs:
+//   bits  0- 7  tl
+//   bits  8-12  D base of the (j, j2) 2x2 node block (fo_owner.cu dmap)
+//   bits 13-14  its (row a, column b) strides: 0 -> (1,1) diagonal block,
+//               1 -> (2,1) for j < j2, 2 -> (1,2) for j > j2
+//   bits 15-19  O index of (row (j,0), column (j2,0)) = 12 j + 2 j2
+//   bits 20-24  O index of (row (j2,0), column (j,0)) = 12 j2 + 2 j (transpose)
+//   bits 25-26  j (residual entry 21 + 2 j + a)
+uint32_t contrib_code(int tl, int j, int j2) {
+  uint32_t dbase, pat;
+  if (j == j2) { dbase = 12 + 3 * j; pat = 0; }
+  else { dbase = 4 * (j + j2 - 1); pat = j < j2 ? 1 : 2; }
+  return uint32_t(tl) | (dbase << 8) | (pat << 13) | (uint32_t(12 * j + 2 * j2) << 15) |
+         (uint32_t(12 * j2 + 2 * j) << 20) | (uint32_t(j) << 25);
+}
 
 // plan of the triangle range [t0, t1)
 void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int32_t t1,
@@ -48,6 +65,7 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
   B.cols.clear();
   B.pairs.clear();
   B.contrib.clear();
+  std::vector<PlanPair> self_pairs;   // appended after the edge pairs (see below)
   std::vector<std::pair<int32_t, int32_t>> inc;   // (column, tl*4 + j)
   for (int32_t t = t0; t < t1; ++t)
     for (int j = 0; j < 3; ++j) inc.push_back({m->tri[size_t(3 * t + j)], (t - t0) * 4 + j});
@@ -62,12 +80,12 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
     const int64_t nc = m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)];
     const int32_t* lst = m->nbr.data() + m->nbr_ptr[size_t(c)];
     const int32_t self = int32_t(std::lower_bound(lst, lst + nc, c) - lst);
-    std::vector<std::vector<uint16_t>> per_slot(static_cast<size_t>(nc));
+    std::vector<std::vector<uint32_t>> per_slot(static_cast<size_t>(nc));
     for (size_t q = i; q < e; ++q) {
       const int32_t tl = inc[q].second >> 2, j = inc[q].second & 3;
       const TriRec& tr = m->trirec[size_t(t0 + tl)];
       for (int j2 = 0; j2 < 3; ++j2)
-        per_slot[tr.slot[3 * j + j2]].push_back(uint16_t((tl << 4) | (j << 2) | j2));
+        per_slot[tr.slot[3 * j + j2]].push_back(contrib_code(tl, j, j2));
     }
     PlanCol pc{};
     pc.colstart = m->colstart[size_t(c)];
@@ -86,17 +104,21 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
       pp.cnt = uint8_t(l.size());
       pp.slot = uint8_t(s);
       pp.col = uint16_t(ci);
-      B.pairs.push_back(pp);
+      if (s == self) self_pairs.push_back(pp); else B.pairs.push_back(pp);
       B.contrib.insert(B.contrib.end(), l.begin(), l.end());
     }
     B.cols.push_back(pc);
     i = e;
   }
+  // Edge slots have 1-2 contributions, self slots one per fan triangle (~6):
+  // edge pairs first (column order, coalesced stores), then the self pairs, so
+  // the lanes of a warp run loops of nearly equal length.
+  B.pairs.insert(B.pairs.end(), self_pairs.begin(), self_pairs.end());
 }
 
 size_t plan_bytes(const PatchBuild& B) {
   return B.cols.size() * sizeof(PlanCol) + B.pairs.size() * sizeof(PlanPair) +
-         ((B.contrib.size() * sizeof(uint16_t) + 15) / 16) * 16;
+         ((B.contrib.size() * sizeof(uint32_t) + 15) / 16) * 16;
 }
 
 }  // namespace
