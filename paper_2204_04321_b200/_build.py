@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(LIB_DIR, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        extra = os.environ.get("FO_EXTRA_NVCC_FLAGS", "").split()
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra, "-Xcompiler", "-fPIC",
                "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",
                "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
         if src.endswith(".cpp"):

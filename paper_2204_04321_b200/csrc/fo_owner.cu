@@ -275,7 +275,9 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
     }
     __syncthreads();
+#ifndef FO_EXPERIMENT_NO_PHASE_B
     phase_b<NEED_J>(sp, k, L, D, O, R, vals);
+#endif
     __syncthreads();
     if (active) {   // the held top block becomes level k+1's diagonal block
       if (NEED_J) {
