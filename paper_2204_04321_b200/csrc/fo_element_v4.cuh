@@ -12,7 +12,7 @@
 //      and the strain-rate coefficients of g = eps_a . grad phi, which is
 //      structured as g_{a,(j,l)} = f_l(zeta) P^a_j + sigma_l r_j Q^a with
 //      P^a_j = e^a_x a_j + e^a_y b_j, Q^a = e^a_z - e^a_x z_x - e^a_y z_y
-//      (stored in the caller's compact scratch `cmp`, 7 values per point);
+//      (stored in the caller's compact scratch `cmp`, 6 values per point);
 //   2. the frozen-viscosity part sum_q c_q H_q comes in closed form from the six
 //      c_q (moments F_ll' = sum c f_l f_l', T2_lj = sum c f_l z_x r_j, T3_jj' =
 //      sum c z_x^2 r_j r_j', ...), exact for the 3 x 2 rule;
@@ -38,7 +38,7 @@ __host__ __device__ constexpr int pk6(int p, int q) {
 
 // Compact per-point storage kept in registers (used by the reference kernels).
 struct RegCmp {
-  double v[42];
+  double v[36];
   __device__ __forceinline__ double& operator()(int i) { return v[i]; }
 };
 
@@ -130,13 +130,14 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   }
   // ---- quadrature loop: compact per-point data
   double cq[6];
-#define dq(q) cmp(7 * (q) + 0)
-#define E1x(q) cmp(7 * (q) + 1)
-#define E1y(q) cmp(7 * (q) + 2)
-#define Qu(q) cmp(7 * (q) + 3)
-#define E2x(q) cmp(7 * (q) + 4)
-#define E2y(q) cmp(7 * (q) + 5)
-#define Qv(q) cmp(7 * (q) + 6)
+  // compact per point q: d, e1x, e1y = e2x = eps_xy, Qu, e2y, Qv (6 values)
+#define dq(q) cmp(6 * (q) + 0)
+#define E1x(q) cmp(6 * (q) + 1)
+#define E1y(q) cmp(6 * (q) + 2)
+#define Qu(q) cmp(6 * (q) + 3)
+#define E2x(q) cmp(6 * (q) + 2)
+#define E2y(q) cmp(6 * (q) + 4)
+#define Qv(q) cmp(6 * (q) + 5)
   {
     const double ex1 = (1.0 - glen_n) / (2.0 * glen_n);
     const double kap = (glen_n - 1.0) / (2.0 * glen_n);
@@ -170,7 +171,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
         Qu(q) = e1z - e1x * zx - e1y * zy;
         Qv(q) = e2z - e2x * zx - e2y * zy;
-        E1x(q) = e1x; E1y(q) = e1y; E2x(q) = e2x; E2y(q) = e2y;
+        E1x(q) = e1x; E1y(q) = e1y; E2y(q) = e2y;   // e2x == e1y
         cq[q] = c;
         dq(q) = d;
       }

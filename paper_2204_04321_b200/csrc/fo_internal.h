@@ -28,8 +28,8 @@ struct alignas(8) TriRec {
 };
 
 // Triangles per patch of the owner-computes kernel (one thread per triangle
-// column, 105 fp64 of shared memory per triangle).
-constexpr int kPatchTris = 120;
+// column, 99 fp64 of shared memory per triangle).
+constexpr int kPatchTris = 128;
 // CTAs resident per SM (2: one CTA's gather phase overlaps the other's
 // element phase)
 constexpr int kPatchCtasPerSm = 2;
@@ -37,7 +37,7 @@ constexpr int kPatchCtasPerSm = 2;
 // entries of one triangle fall in different banks
 constexpr int kPatchStride = kPatchTris + 1;
 // shared-memory budget of one patch's plan (columns, pairs, contributions)
-constexpr int kPlanBytes = (233472 - 1024 * kPatchCtasPerSm) / kPatchCtasPerSm - 105 * kPatchStride * 8 - 64;
+constexpr int kPlanBytes = (233472 - 1024 * kPatchCtasPerSm) / kPatchCtasPerSm - 99 * kPatchStride * 8 - 64;
 
 // plan records (fo_plan.cpp); copied to shared memory by the kernel
 struct PlanCol {            // 24 bytes

@@ -42,7 +42,7 @@ struct PlanView {
 constexpr int TP = kPatchStride;   // SoA row stride (threads per CTA: kPatchTris)
 constexpr int kD = 27;   // level-k diagonal block (21, 2x2-block layout) + 6 residual
 constexpr int kO = 36;   // 6x6 bottom-top block of wedge k
-constexpr int kC = 42;   // compact per-point scratch (7 x 6 quadrature points)
+constexpr int kC = 36;   // compact per-point scratch (6 x 6 quadrature points)
 constexpr int kSlotsPerTri = kD + kO + kC;
 
 // D layout: the three off-diagonal 2x2 node blocks (j < j2) first, row-major
@@ -66,6 +66,13 @@ struct SmemPlan {
 };
 
 __device__ __forceinline__ void put2(double* dst, double x, double y, bool interior) {
+#ifdef FO_EXPERIMENT_NO_RED
+  interior = true;
+#endif
+#ifdef FO_EXPERIMENT_NO_STORE
+  if (x == 1.2345e300 && y == -1.0) { *dst = x; }   // keep the sums alive, store nothing
+  return;
+#endif
   if (interior) {
     *reinterpret_cast<double2*>(dst) = make_double2(x, y);
   } else {
@@ -78,17 +85,17 @@ __device__ __forceinline__ void put2(double* dst, double x, double y, bool inter
 // One thread per (column, slot) pair walks the slot's contributions once and
 // gathers: level-kk rows, column level kk (from D) and kk+1 (from O); level
 // kk+1 rows, column level kk (from O transposed).  The level-kk rows' column
-// level kk-1 part was written by the previous call (partial rows, merged in
-// L2).  Pairs are ordered by contribution count in the plan, so the lanes of a
-// warp run loops of (nearly) equal length.  Then one thread per column
-// gathers the residual of node (c, kk) from the self slot.
+// level kk-1 part was written by the previous call (partial rows, completed
+// in L2).  Edge pairs (1-2 contributions) come first in the plan, self pairs
+// (one contribution per fan triangle) last, so loop lengths in a warp are
+// nearly uniform; consecutive slots of a column sit on consecutive lanes.
 template <bool UP>
 __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
                                           const double* O, double* __restrict__ vals) {
-  const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // groups of level-kk rows
-  const int m1 = (kk + 1 == L) ? 2 : 3;                   // groups of level-kk+1 rows
+  const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // column groups of level-kk rows
+  const int m1 = (kk + 1 == L) ? 2 : 3;                   // column groups of level-kk+1 rows
   const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
-  const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk row slot
+  const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk-row slot
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
     const PlanCol& pc = sp.cols[pp.col];
@@ -96,7 +103,11 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
     double up00 = 0.0, up01 = 0.0, up10 = 0.0, up11 = 0.0;
     double nx00 = 0.0, nx01 = 0.0, nx10 = 0.0, nx11 = 0.0;
     const uint32_t* cp = sp.contrib + pp.off;
+#ifdef FO_EXPERIMENT_NO_GATHER
+    for (int e = 0; e < 0; ++e) {
+#else
     for (int e = 0; e < pp.cnt; ++e) {
+#endif
       const uint32_t cb = cp[e];
       const int tl = int(cb & 255);
       const int pat = int((cb >> 13) & 3);
@@ -121,8 +132,7 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
     }
     const int nc = pc.info & 255;
     const bool interior = (pc.info >> 8) & 1;
-    const int64_t seg0 = pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
-    double* d0 = vals + seg0;
+    double* d0 = vals + pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
     double* d1 = d0 + 2 * nc * m0;
     put2(d0, dg00, dg01, interior);
     put2(d1, dg10, dg11, interior);
