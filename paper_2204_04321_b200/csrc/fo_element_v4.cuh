@@ -23,8 +23,9 @@
 // Sink interface (local DOF p = 2 j + comp of one level):
 //   r_bot_add(p, v)           residual, bottom nodes
 //   bot_add(p, p2, v)         (bottom, bottom) block, p <= p2
-//   off(p, p2, v) / off_add   (bottom, top) block (first write, then adds)
-//   top(i, v) / top_add       (top, top) block (i = pk6 packed), first write
+//   bot_get / bot_set         (bottom, bottom) read-back / overwrite
+//   off(p, p2, v) / off_get   (bottom, top) block write / read-back
+//   top(i, v) / top_get       (top, top) block (i = pk6 packed) write / read-back
 //   r_top(p, v) / r_top_add   top residual (first write, then adds)
 #pragma once
 
@@ -241,30 +242,37 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       }
   }
   // frozen-viscosity entry: row comp ca of node (j,l), column comp cb of node (j2,l2)
+  // scaled barycentric gradients (the 2 and 1/2 of the strain-rate vectors)
+  double a2[3], ah[3], b2[3], bh[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    a2[j] = 2.0 * w.a[j]; ah[j] = 0.5 * w.a[j];
+    b2[j] = 2.0 * w.b[j]; bh[j] = 0.5 * w.b[j];
+  }
   auto hpart = [&](int ca, int j, int l, int cb, int j2, int l2) -> double {
     const double sg = l == 0 ? -1.0 : 1.0, sg2 = l2 == 0 ? -1.0 : 1.0;
     const double Fv = F[l + l2];
     const int kk = j <= j2 ? (j * 3 - (j * (j - 1)) / 2 + (j2 - j)) : (j2 * 3 - (j2 * (j2 - 1)) / 2 + (j - j2));
     const double aj = w.a[j], bj = w.b[j], aj2 = w.a[j2], bj2 = w.b[j2];
     if (ca == 0 && cb == 0) {
-      const double AA = fma(2.0 * aj, aj2, 0.5 * bj * bj2);
-      const double G1 = fma(2.0 * aj, T2x[l][j2], 0.5 * bj * T2y[l][j2]);
-      const double G2 = fma(2.0 * aj2, T2x[l2][j], 0.5 * bj2 * T2y[l2][j]);
+      const double AA = fma(a2[j], aj2, bh[j] * bj2);
+      const double G1 = fma(a2[j], T2x[l][j2], bh[j] * T2y[l][j2]);
+      const double G2 = fma(a2[j2], T2x[l2][j], bh[j2] * T2y[l2][j]);
       return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKuu[kk])));
     } else if (ca == 1 && cb == 1) {
-      const double AA = fma(0.5 * aj, aj2, 2.0 * bj * bj2);
-      const double G1 = fma(0.5 * aj, T2x[l][j2], 2.0 * bj * T2y[l][j2]);
-      const double G2 = fma(0.5 * aj2, T2x[l2][j], 2.0 * bj2 * T2y[l2][j]);
+      const double AA = fma(ah[j], aj2, b2[j] * bj2);
+      const double G1 = fma(ah[j], T2x[l][j2], b2[j] * T2y[l][j2]);
+      const double G2 = fma(ah[j2], T2x[l2][j], b2[j2] * T2y[l2][j]);
       return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKvv[kk])));
     } else if (ca == 0) {   // row u(j,l), column v(j2,l2)
-      const double AA = fma(aj, bj2, 0.5 * aj2 * bj);
-      const double G1 = fma(aj, T2y[l][j2], 0.5 * bj * T2x[l][j2]);
-      const double G2 = fma(bj2, T2x[l2][j], 0.5 * aj2 * T2y[l2][j]);
+      const double AA = fma(aj, bj2, ah[j2] * bj);
+      const double G1 = fma(aj, T2y[l][j2], bh[j] * T2x[l][j2]);
+      const double G2 = fma(bj2, T2x[l2][j], ah[j2] * T2y[l2][j]);
       return fma(Fv, AA, fma(-sg2, G1, fma(-sg, G2, sg * sg2 * KKuv[kk])));
     } else {                // row v(j,l), column u(j2,l2) = J_{u(j2,l2), v(j,l)}
-      const double AA = fma(aj2, bj, 0.5 * aj * bj2);
-      const double G1 = fma(aj2, T2y[l2][j], 0.5 * bj2 * T2x[l2][j]);
-      const double G2 = fma(bj, T2x[l][j2], 0.5 * aj * T2y[l][j2]);
+      const double AA = fma(aj2, bj, ah[j] * bj2);
+      const double G1 = fma(aj2, T2y[l2][j], bh[j2] * T2x[l2][j]);
+      const double G2 = fma(bj, T2x[l][j2], ah[j] * T2y[l][j2]);
       return fma(Fv, AA, fma(-sg, G1, fma(-sg2, G2, sg * sg2 * KKuv[kk])));
     }
   };
@@ -299,12 +307,14 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
           }
       }
   }
-  if (w.go) {   // rank-1 (bottom, top)
+  if (w.go) {   // rank-1 (bottom, top), accumulated onto the frozen-viscosity part
     double acc[36];
 #pragma unroll
-    for (int i = 0; i < 36; ++i) acc[i] = 0.0;
-#pragma unroll 1
-    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
+#pragma unroll 2
+    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
       const double zeta = (q & 1) ? kZeta : -kZeta;
@@ -329,17 +339,19 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
-      for (int p2 = 0; p2 < 6; ++p2) sink.off_add(p, p2, acc[6 * p + p2]);
+      for (int p2 = 0; p2 < 6; ++p2) sink.off(p, p2, acc[6 * p + p2]);
     gate = acc[35];
   }
   if (w.go) {   // rank-1 (bottom, bottom) and the bottom viscous residual
     double acc[21], res[6];
 #pragma unroll
-    for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = sink.bot_get(p, p2);
 #pragma unroll
     for (int i = 0; i < 6; ++i) res[i] = 0.0;
-#pragma unroll 1
-    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+#pragma unroll 2
+    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
       const double zeta = (q & 1) ? kZeta : -kZeta;
@@ -366,7 +378,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
-      for (int p2 = p; p2 < 6; ++p2) sink.bot_add(p, p2, acc[pk6(p, p2)]);
+      for (int p2 = p; p2 < 6; ++p2) sink.bot_set(p, p2, acc[pk6(p, p2)]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) sink.r_bot_add(p, res[p]);
     gate = acc[20];
@@ -374,11 +386,11 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   if (w.go) {   // rank-1 (top, top), added to the held block; the top viscous residual
     double acc[21], res[6];
 #pragma unroll
-    for (int i = 0; i < 21; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 21; ++i) acc[i] = sink.top_get(i);
 #pragma unroll
     for (int i = 0; i < 6; ++i) res[i] = 0.0;
-#pragma unroll 1
-    for (int q = 0; q < 6; ++q) {   // rolled: one point's data live at a time
+#pragma unroll 2
+    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
       const double zeta = (q & 1) ? kZeta : -kZeta;
@@ -403,7 +415,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = fma(-dg[p], g[p2], acc[pk6(p, p2)]);
     }
 #pragma unroll
-    for (int i = 0; i < 21; ++i) sink.top_add(i, acc[i]);
+    for (int i = 0; i < 21; ++i) sink.top(i, acc[i]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) sink.r_top_add(p, res[p]);
   }

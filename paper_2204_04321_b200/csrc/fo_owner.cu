@@ -183,6 +183,18 @@ struct PatchSink {
   __device__ __forceinline__ void bot_add(int p, int p2, double v) { D[dmap(p, p2) * TP + tl] += v; }
   __device__ __forceinline__ void off(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] = v; }
   __device__ __forceinline__ void off_add(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] += v; }
+  __device__ __forceinline__ double off_get(int p, int p2) const { return O[(6 * p + p2) * TP + tl]; }
+  __device__ __forceinline__ double bot_get(int p, int p2) const { return D[dmap(p, p2) * TP + tl]; }
+  __device__ __forceinline__ void bot_set(int p, int p2, double v) { D[dmap(p, p2) * TP + tl] = v; }
+  __device__ __forceinline__ double top_get(int i) const {
+    double v = 0.0;
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = p; p2 < 6; ++p2)
+        if (pk6(p, p2) == i) v = held[dmap(p, p2)];
+    return v;
+  }
   __device__ __forceinline__ void top(int i, double v) {
     // i is the packed upper-triangle index pk6(p, p2)
 #pragma unroll
@@ -211,6 +223,10 @@ struct PatchSinkR {
   __device__ __forceinline__ void bot_add(int, int, double) {}
   __device__ __forceinline__ void off(int, int, double) {}
   __device__ __forceinline__ void off_add(int, int, double) {}
+  __device__ __forceinline__ double off_get(int, int) const { return 0.0; }
+  __device__ __forceinline__ double bot_get(int, int) const { return 0.0; }
+  __device__ __forceinline__ void bot_set(int, int, double) {}
+  __device__ __forceinline__ double top_get(int) const { return 0.0; }
   __device__ __forceinline__ void top(int, double) {}
   __device__ __forceinline__ void top_add(int, double) {}
   __device__ __forceinline__ void r_top(int p, double v) { held[21 + p] = v; }
