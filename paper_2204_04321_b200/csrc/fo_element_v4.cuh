@@ -342,82 +342,62 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       for (int p2 = 0; p2 < 6; ++p2) sink.off(p, p2, acc[6 * p + p2]);
     gate = acc[35];
   }
-  if (w.go) {   // rank-1 (bottom, bottom) and the bottom viscous residual
-    double acc[21], res[6];
+  if (w.go) {   // rank-1 (bottom, bottom) and (top, top) in one pass, with both
+                //   viscous residual halves; (top, top) onto the held block
+    double ab[21], at[21], rb[6], rt[6];
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
-      for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = sink.bot_get(p, p2);
+      for (int p2 = p; p2 < 6; ++p2) ab[pk6(p, p2)] = sink.bot_get(p, p2);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) res[i] = 0.0;
-#pragma unroll 2
-    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
+    for (int i = 0; i < 21; ++i) at[i] = sink.top_get(i);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) rb[i] = rt[i] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
       const double zeta = (q & 1) ? kZeta : -kZeta;
-      const double f0 = 0.5 - 0.5 * zeta;
+      const double f0 = 0.5 - 0.5 * zeta, f1 = 0.5 + 0.5 * zeta;
       const double dd = fma(0.0, gate, dq(q));
-      double g[6], dg[6];
+      const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
+      double gb[6], gt[6], dgb[6], dgt[6];
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
-        g[2 * j] = fma(f0, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), -rj * Qu(q));
-        g[2 * j + 1] = fma(f0, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), -rj * Qv(q));
+        const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
+        const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
+        const double qu = rj * Qu(q), qv = rj * Qv(q);
+        gb[2 * j] = fma(f0, pu, -qu);
+        gb[2 * j + 1] = fma(f0, pv, -qv);
+        gt[2 * j] = fma(f1, pu, qu);
+        gt[2 * j + 1] = fma(f1, pv, qv);
       }
-      const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
-        dg[p] = dd * g[p];
-        res[p] = fma(cc, g[p], res[p]);   // R_{a,(j,0)} += c_q g
+        dgb[p] = dd * gb[p];
+        dgt[p] = dd * gt[p];
+        rb[p] = fma(cc, gb[p], rb[p]);   // R_{a,(j,0)} += c_q g
+        rt[p] = fma(cc, gt[p], rt[p]);   // R_{a,(j,1)} += c_q g
       }
 #pragma unroll
       for (int p = 0; p < 6; ++p)
 #pragma unroll
-        for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = fma(-dg[p], g[p2], acc[pk6(p, p2)]);
+        for (int p2 = p; p2 < 6; ++p2) {
+          ab[pk6(p, p2)] = fma(-dgb[p], gb[p2], ab[pk6(p, p2)]);
+          at[pk6(p, p2)] = fma(-dgt[p], gt[p2], at[pk6(p, p2)]);
+        }
     }
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
-      for (int p2 = p; p2 < 6; ++p2) sink.bot_set(p, p2, acc[pk6(p, p2)]);
+      for (int p2 = p; p2 < 6; ++p2) sink.bot_set(p, p2, ab[pk6(p, p2)]);
 #pragma unroll
-    for (int p = 0; p < 6; ++p) sink.r_bot_add(p, res[p]);
-    gate = acc[20];
-  }
-  if (w.go) {   // rank-1 (top, top), added to the held block; the top viscous residual
-    double acc[21], res[6];
+    for (int p = 0; p < 6; ++p) sink.r_bot_add(p, rb[p]);
 #pragma unroll
-    for (int i = 0; i < 21; ++i) acc[i] = sink.top_get(i);
+    for (int i = 0; i < 21; ++i) sink.top(i, at[i]);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) res[i] = 0.0;
-#pragma unroll 2
-    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
-      const int a = q >> 1;
-      const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
-      const double zeta = (q & 1) ? kZeta : -kZeta;
-      const double f1 = 0.5 + 0.5 * zeta;
-      const double dd = fma(0.0, gate, dq(q));
-      double g[6], dg[6];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
-        g[2 * j] = fma(f1, fma(E1x(q), w.a[j], E1y(q) * w.b[j]), rj * Qu(q));
-        g[2 * j + 1] = fma(f1, fma(E2x(q), w.a[j], E2y(q) * w.b[j]), rj * Qv(q));
-      }
-      const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        dg[p] = dd * g[p];
-        res[p] = fma(cc, g[p], res[p]);   // R_{a,(j,1)} += c_q g
-      }
-#pragma unroll
-      for (int p = 0; p < 6; ++p)
-#pragma unroll
-        for (int p2 = p; p2 < 6; ++p2) acc[pk6(p, p2)] = fma(-dg[p], g[p2], acc[pk6(p, p2)]);
-    }
-#pragma unroll
-    for (int i = 0; i < 21; ++i) sink.top(i, acc[i]);
-#pragma unroll
-    for (int p = 0; p < 6; ++p) sink.r_top_add(p, res[p]);
+    for (int p = 0; p < 6; ++p) sink.r_top_add(p, rt[p]);
   }
 #undef dq
 #undef E1x
