@@ -31,6 +31,15 @@
 
 #include "fo_element.cuh"
 
+#ifndef FO_UNROLL_R1A
+#define FO_UNROLL_R1A 2   // trips of the (bottom, top) rank-1 loop unrolled
+#endif
+#ifndef FO_UNROLL_R1B
+#define FO_UNROLL_R1B 2   // trips of the merged (bottom,bottom)+(top,top) loop unrolled
+#endif
+#define FO_PRAGMA(x) _Pragma(#x)
+#define FO_UNROLL(n) FO_PRAGMA(unroll n)
+
 namespace fo {
 
 __host__ __device__ constexpr int pk6(int p, int q) {
@@ -313,8 +322,8 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     for (int p = 0; p < 6; ++p)
 #pragma unroll
       for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
-#pragma unroll 2
-    for (int q = 0; q < 6; ++q) {   // two points per trip: ILP without all six live
+FO_UNROLL(FO_UNROLL_R1A)
+    for (int q = 0; q < 6; ++q) {   // rolled: not all six points' data live at once
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
       const double zeta = (q & 1) ? kZeta : -kZeta;
@@ -353,7 +362,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     for (int i = 0; i < 21; ++i) at[i] = sink.top_get(i);
 #pragma unroll
     for (int i = 0; i < 6; ++i) rb[i] = rt[i] = 0.0;
-#pragma unroll 1
+FO_UNROLL(FO_UNROLL_R1B)
     for (int q = 0; q < 6; ++q) {
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
