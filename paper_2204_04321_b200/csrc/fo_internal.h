@@ -43,11 +43,22 @@ constexpr int kPlanBytes = (233472 - 1024 * kPatchCtasPerSm) / kPatchCtasPerSm -
 struct PlanCol {            // 24 bytes
   int64_t colstart;         // CSR value offset of the column's first row
   int32_t c;                // local column id
-  int32_t info;             // n_c | interior << 8 | self slot << 9
+  int32_t info;             // n_c | interior << 8 | self slot << 9 | multi << 30
   uint16_t self_off;        // contributions of the self slot (residual)
   uint16_t self_cnt;
-  uint32_t pad;
+  uint32_t pad;             // multi columns: this patch's partial block
 };
+// a column touched by >= 3 patches: self-slot and residual partial sums go to
+// partial blocks base .. base + cnt - 1 (patch order), summed by the fix-up pass
+struct MultiRec {           // 24 bytes
+  int64_t colstart;
+  int32_t c;
+  int32_t nc_self;          // n_c | self slot << 8
+  int32_t base;
+  int32_t cnt;
+};
+// doubles per (partial block, level): dg 4, up 4, nx 4, residual 2 (+2 pad)
+constexpr int kPartialStride = 16;
 struct PlanPair {           // 8 bytes: one (column, slot) of phase B
   uint16_t off;             // first contribution (patch-relative)
   uint8_t cnt;              // number of contributions
@@ -68,6 +79,8 @@ struct PatchPlan {
   std::vector<PlanPair> pairs;
   std::vector<uint32_t> contrib;     // encoded contribution (fo_plan.cpp contrib_code)
   std::vector<int32_t> zero_cols;    // boundary columns (zero-filled before the kernel)
+  std::vector<MultiRec> multi;       // columns touched by >= 3 patches
+  int32_t n_partials = 0;
 };
 
 struct DevPatch {
@@ -79,6 +92,8 @@ struct DevPatch {
   PlanPair* pairs = nullptr;
   uint32_t* contrib = nullptr;
   int32_t* zero_cols = nullptr;
+  MultiRec* multi = nullptr;
+  double* partials = nullptr;        // [n_partials][L+1][kPartialStride]
 };
 
 }  // namespace fo

@@ -37,6 +37,7 @@ struct PlanView {
   const PlanCol* __restrict__ cols;
   const PlanPair* __restrict__ pairs;
   const uint32_t* __restrict__ contrib;
+  double* partials;   // multi columns' partial blocks (fo_plan.cpp)
 };
 
 constexpr int TP = kPatchStride;   // SoA row stride (threads per CTA: kPatchTris)
@@ -91,7 +92,8 @@ __device__ __forceinline__ void put2(double* dst, double x, double y, bool inter
 // nearly uniform; consecutive slots of a column sit on consecutive lanes.
 template <bool UP>
 __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
-                                          const double* O, double* __restrict__ vals) {
+                                          const double* O, double* __restrict__ vals,
+                                          double* __restrict__ partials) {
   const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // column groups of level-kk rows
   const int m1 = (kk + 1 == L) ? 2 : 3;                   // column groups of level-kk+1 rows
   const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
@@ -132,6 +134,19 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
     }
     const int nc = pc.info & 255;
     const bool interior = (pc.info >> 8) & 1;
+    if (((pc.info >> 30) & 1) && pp.slot == ((pc.info >> 9) & 255)) {
+      // self slot of a multi column: this patch's partial block
+      double2* q = reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride);
+      q[0] = make_double2(dg00, dg01);
+      q[1] = make_double2(dg10, dg11);
+      if (UP) {
+        q[2] = make_double2(up00, up01);
+        q[3] = make_double2(up10, up11);
+        q[4] = make_double2(nx00, nx01);
+        q[5] = make_double2(nx10, nx11);
+      }
+      continue;
+    }
     double* d0 = vals + pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
     double* d1 = d0 + 2 * nc * m0;
     put2(d0, dg00, dg01, interior);
@@ -147,7 +162,7 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
 }
 
 __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, const double* D,
-                                          double* __restrict__ R) {
+                                          double* __restrict__ R, double* __restrict__ partials) {
   for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
     const PlanCol& pc = sp.cols[ci];
     double r0 = 0.0, r1 = 0.0;
@@ -157,19 +172,23 @@ __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, con
       r0 += Dr[0];
       r1 += Dr[TP];
     }
-    put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
+    if ((pc.info >> 30) & 1)
+      *reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride + 12) =
+          make_double2(r0, r1);
+    else
+      put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
   }
 }
 
 template <bool NEED_J>
 __device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const double* D,
                                         const double* O, double* __restrict__ R,
-                                        double* __restrict__ vals) {
+                                        double* __restrict__ vals, double* __restrict__ partials) {
   if (NEED_J) {
-    if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals);
-    else phase_b_j<false>(sp, kk, L, D, O, vals);
+    if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals, partials);
+    else phase_b_j<false>(sp, kk, L, D, O, vals, partials);
   }
-  phase_b_r(sp, kk, L, D, R);
+  phase_b_r(sp, kk, L, D, R, partials);
 }
 
 // Sink of wedge_element_v4: bottom parts added to D and O in shared memory,
@@ -302,7 +321,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     }
     __syncthreads();
 #ifndef FO_EXPERIMENT_NO_PHASE_B
-    phase_b<NEED_J>(sp, k, L, D, O, R, vals);
+    phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials);
 #endif
     __syncthreads();
     if (active) {   // the held top block becomes level k+1's diagonal block
@@ -316,7 +335,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     }
   }
   __syncthreads();
-  phase_b<NEED_J>(sp, L, L, D, O, R, vals);
+  phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials);
 }
 
 // zero the rows (CSR values and residual) of boundary columns
@@ -337,6 +356,51 @@ __global__ void zero_boundary_kernel(const ColRec* __restrict__ col, const int32
   }
 }
 
+// multi columns: add the patches' partial blocks in patch order and store the
+// self-slot entries and the residual (one thread per column and row level)
+__global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L,
+                                   const double* __restrict__ partials, double* __restrict__ R,
+                                   double* __restrict__ vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * (L + 1)) return;
+  const int mc = i / (L + 1), kk = i - mc * (L + 1);
+  const MultiRec r = mr[mc];
+  const bool up = vals && kk < L;
+  double s[14];
+#pragma unroll
+  for (int e = 0; e < 14; ++e) s[e] = 0.0;
+  for (int b = 0; b < r.cnt; ++b) {
+    const double* q = partials + (int64_t(r.base + b) * (L + 1) + kk) * kPartialStride;
+    s[12] += q[12];
+    s[13] += q[13];
+    if (vals) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[e] += q[e];
+    }
+    if (up) {
+#pragma unroll
+      for (int e = 4; e < 12; ++e) s[e] += q[e];
+    }
+  }
+  *reinterpret_cast<double2*>(R + 2 * (int64_t(r.c) * (L + 1) + kk)) = make_double2(s[12], s[13]);
+  if (!vals) return;
+  const int nc = r.nc_self & 255, slot = r.nc_self >> 8;
+  const int m0 = (kk == 0 || kk == L) ? 2 : 3, m1 = (kk + 1 == L) ? 2 : 3;
+  const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
+  const int g0 = kk == 0 ? 0 : 2;
+  double* d0 = vals + r.colstart + int64_t(4 * nc) * P0 + int64_t(slot) * (2 * m0) + g0;
+  double* d1 = d0 + 2 * nc * m0;
+  *reinterpret_cast<double2*>(d0) = make_double2(s[0], s[1]);
+  *reinterpret_cast<double2*>(d1) = make_double2(s[2], s[3]);
+  if (up) {
+    *reinterpret_cast<double2*>(d0 + 2) = make_double2(s[4], s[5]);
+    *reinterpret_cast<double2*>(d1 + 2) = make_double2(s[6], s[7]);
+    double* e0 = vals + r.colstart + int64_t(4 * nc) * P1 + int64_t(slot) * (2 * m1);
+    *reinterpret_cast<double2*>(e0) = make_double2(s[8], s[9]);
+    *reinterpret_cast<double2*>(e0 + 2 * nc * m1) = make_double2(s[10], s[11]);
+  }
+}
+
 static size_t smem_bytes(bool) { return size_t(kSlotsPerTri) * TP * sizeof(double) + kPlanBytes; }
 
 template <bool NEED_J, bool N3>
@@ -351,7 +415,7 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     attr_set = true;
   }
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.contrib_ptr,
-              m->d_plan.cols, m->d_plan.pairs, m->d_plan.contrib};
+              m->d_plan.cols, m->d_plan.pairs, m->d_plan.contrib, m->d_plan.partials};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
@@ -401,7 +465,17 @@ fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals
   else
     st = n3 ? launch_patch<false, true>(m, d_U, R, nullptr, s) : launch_patch<false, false>(m, d_U, R, nullptr, s);
   if (st) return st;
-  m->last_launches = launches + 1;
+  ++launches;
+  const int nm = int(m->plan.multi.size());
+  if (nm > 0) {
+    const int n = nm * (m->L + 1);
+    multi_fixup_kernel<<<(n + 127) / 128, 128, 0, s>>>(m->d_plan.multi, nm, m->L, m->d_plan.partials, R,
+                                                       need_j ? d_vals : nullptr);
+    st = cuda_status(cudaGetLastError(), "multi_fixup_kernel launch");
+    if (st) return st;
+    ++launches;
+  }
+  m->last_launches = launches;
   return FO_OK;
 }
 

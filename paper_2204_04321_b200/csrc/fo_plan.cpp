@@ -14,7 +14,11 @@
 // fan: its rows are written with plain stores (every slot, zeros included).
 // Otherwise it is a BOUNDARY column: its rows are zero-filled before the
 // kernel and every touching patch adds its partial sums with fp64 RED, for
-// the slots it contributes to only.
+// the slots it contributes to only.  Two partial sums added onto zero give
+// the same double in either order; where three or more patches touch a column
+// (its self slot and residual collect all of them), each patch instead stores
+// its partial sums to a scratch block of its own and a fix-up pass adds them
+// in patch order, so the assembly is bitwise reproducible.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -173,6 +177,33 @@ fo_status build_patch_plan(fo_mesh m) {
   P.n_patches = int32_t(P.t_begin.size() - 1);
   for (int64_t c = 0; c < nk; ++c)
     if (boundary[size_t(c)]) P.zero_cols.push_back(int32_t(c));
+  // MULTI columns: touched by >= 3 patches; partial block b = base + rank
+  // (rank = order of the patch among the column's patches)
+  {
+    std::vector<int32_t> touch(size_t(m->n_col), 0), base(size_t(m->n_col), -1), next(size_t(m->n_col), 0);
+    for (const PlanCol& pc : P.cols) touch[size_t(pc.c)]++;
+    int32_t nb = 0;
+    for (const PlanCol& pc : P.cols) {
+      const int32_t c = pc.c;
+      if (touch[size_t(c)] >= 3 && base[size_t(c)] < 0) {
+        base[size_t(c)] = nb;
+        nb += touch[size_t(c)];
+        MultiRec mr{};
+        mr.colstart = pc.colstart;
+        mr.c = c;
+        mr.nc_self = (pc.info & 255) | (((pc.info >> 9) & 255) << 8);
+        mr.base = base[size_t(c)];
+        mr.cnt = touch[size_t(c)];
+        P.multi.push_back(mr);
+      }
+    }
+    for (PlanCol& pc : P.cols)   // patches in order: ranks ascend with the patch index
+      if (base[size_t(pc.c)] >= 0) {
+        pc.info |= 1 << 30;
+        pc.pad = uint32_t(base[size_t(pc.c)] + next[size_t(pc.c)]++);
+      }
+    P.n_partials = nb;
+  }
   fo_status st = upload_vec(&m->d_plan.t_begin, P.t_begin);
   if (!st) st = upload_vec(&m->d_plan.col_ptr, P.col_ptr);
   if (!st) st = upload_vec(&m->d_plan.pair_ptr, P.pair_ptr);
@@ -181,6 +212,11 @@ fo_status build_patch_plan(fo_mesh m) {
   if (!st) st = upload_vec(&m->d_plan.pairs, P.pairs);
   if (!st) st = upload_vec(&m->d_plan.contrib, P.contrib);
   if (!st) st = upload_vec(&m->d_plan.zero_cols, P.zero_cols);
+  if (!st) st = upload_vec(&m->d_plan.multi, P.multi);
+  if (!st && P.n_partials > 0)
+    st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.partials),
+                                sizeof(double) * kPartialStride * size_t(m->L + 1) * size_t(P.n_partials)),
+                     "cudaMalloc");
   return st;
 }
 
