@@ -92,6 +92,8 @@ struct DevPatch {
   PlanPair* pairs = nullptr;
   uint32_t* contrib = nullptr;
   int32_t* zero_cols = nullptr;
+  uint8_t* blob = nullptr;           // per-patch plan blobs (shared-memory layout)
+  int64_t* blob_off = nullptr;       // [n_patches+1] byte offsets, multiples of 16
   MultiRec* multi = nullptr;
   double* partials = nullptr;        // [n_partials][L+1][kPartialStride]
 };

@@ -33,18 +33,36 @@ struct PlanView {
   const int32_t* __restrict__ t_begin;
   const int32_t* __restrict__ col_ptr;
   const int32_t* __restrict__ pair_ptr;
-  const int64_t* __restrict__ contrib_ptr;
-  const PlanCol* __restrict__ cols;
-  const PlanPair* __restrict__ pairs;
-  const uint32_t* __restrict__ contrib;
+  const uint8_t* __restrict__ blob;      // per-patch plan blobs (fo_plan.cpp)
+  const int64_t* __restrict__ blob_off;
   double* partials;   // multi columns' partial blocks (fo_plan.cpp)
 };
+
+// one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(b) : "memory");
+}
 
 constexpr int TP = kPatchStride;   // SoA row stride (threads per CTA: kPatchTris)
 constexpr int kD = 27;   // level-k diagonal block (21, 2x2-block layout) + 6 residual
 constexpr int kO = 36;   // 6x6 bottom-top block of wedge k
 constexpr int kC = 36;   // compact per-point scratch (6 x 6 quadrature points)
 constexpr int kSlotsPerTri = kD + kO + kC;
+// byte offset of the plan in dynamic shared memory (16-byte aligned for the bulk copy)
+constexpr int kPlanOffset = (kSlotsPerTri * TP * 8 + 15) / 16 * 16;
 
 // D layout: the three off-diagonal 2x2 node blocks (j < j2) first, row-major
 // [a][b], at 4 (j + j2 - 1); then the three diagonal node blocks (a <= b) at
@@ -265,29 +283,26 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
                 const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
                 PlanView pv, const double* __restrict__ U, double* __restrict__ R,
                 double* __restrict__ vals) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   double* const D = smem;                    // [kD][TP]
   double* const O = smem + kD * TP;          // [kO][TP]
   double* const C = smem + (kD + kO) * TP;   // [kC][TP]
   const int p = blockIdx.x;
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
-  // the patch's plan -> shared memory (after the value buffers)
+  // the patch's plan -> shared memory (after the value buffers): one bulk
+  // copy, issued now and waited for before the first gather phase
+  __shared__ uint64_t plan_bar;
   SmemPlan sp;
   {
     const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
     const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
-    const int64_t e0 = __ldg(pv.contrib_ptr + p), e1 = __ldg(pv.contrib_ptr + p + 1);
-    char* base = reinterpret_cast<char*>(smem + kSlotsPerTri * TP);
-    PlanCol* cs = reinterpret_cast<PlanCol*>(base);
-    PlanPair* ps = reinterpret_cast<PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
-    uint32_t* es = reinterpret_cast<uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
-    for (int i = threadIdx.x; i < (c1 - c0) * int(sizeof(PlanCol) / 8); i += blockDim.x)
-      reinterpret_cast<int2*>(cs)[i] = __ldg(reinterpret_cast<const int2*>(pv.cols + c0) + i);
-    for (int i = threadIdx.x; i < q1 - q0; i += blockDim.x)
-      reinterpret_cast<int2*>(ps)[i] = __ldg(reinterpret_cast<const int2*>(pv.pairs + q0) + i);
-    for (int i = threadIdx.x; i < int(e1 - e0); i += blockDim.x) es[i] = __ldg(pv.contrib + e0 + i);
-    sp.cols = cs; sp.pairs = ps; sp.contrib = es;
+    const int64_t b0 = __ldg(pv.blob_off + p), b1 = __ldg(pv.blob_off + p + 1);
+    char* base = reinterpret_cast<char*>(smem) + kPlanOffset;
+    sp.cols = reinterpret_cast<const PlanCol*>(base);
+    sp.pairs = reinterpret_cast<const PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
+    sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
     sp.ncols = c1 - c0; sp.npairs = q1 - q0;
+    if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
   const int L = kp.L;
   const int tl = threadIdx.x;
@@ -319,6 +334,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       SmemCmp cmp{C, tl};
       wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
     }
+    if (k == 0) bulk_wait(&plan_bar);
     __syncthreads();
 #ifndef FO_EXPERIMENT_NO_PHASE_B
     phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials);
@@ -334,6 +350,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       }
     }
   }
+  if (L == 0) bulk_wait(&plan_bar);
   __syncthreads();
   phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials);
 }
@@ -401,7 +418,7 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
   }
 }
 
-static size_t smem_bytes(bool) { return size_t(kSlotsPerTri) * TP * sizeof(double) + kPlanBytes; }
+static size_t smem_bytes(bool) { return size_t(kPlanOffset) + kPlanBytes; }
 
 template <bool NEED_J, bool N3>
 static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
@@ -414,8 +431,8 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     if (st) return st;
     attr_set = true;
   }
-  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.contrib_ptr,
-              m->d_plan.cols, m->d_plan.pairs, m->d_plan.contrib, m->d_plan.partials};
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr,
+              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);

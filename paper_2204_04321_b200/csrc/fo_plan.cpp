@@ -204,13 +204,28 @@ fo_status build_patch_plan(fo_mesh m) {
       }
     P.n_partials = nb;
   }
+  // one 16-byte aligned blob per patch in the shared-memory layout of the
+  // kernel (columns | pairs | contributions), copied with one bulk copy
+  std::vector<uint8_t> blob;
+  std::vector<int64_t> blob_off(1, 0);
+  for (int32_t p = 0; p < P.n_patches; ++p) {
+    auto put = [&](const void* src, size_t n) {
+      const uint8_t* b = static_cast<const uint8_t*>(src);
+      blob.insert(blob.end(), b, b + n);
+    };
+    put(P.cols.data() + P.col_ptr[size_t(p)], sizeof(PlanCol) * size_t(P.col_ptr[size_t(p) + 1] - P.col_ptr[size_t(p)]));
+    put(P.pairs.data() + P.pair_ptr[size_t(p)],
+        sizeof(PlanPair) * size_t(P.pair_ptr[size_t(p) + 1] - P.pair_ptr[size_t(p)]));
+    put(P.contrib.data() + P.contrib_ptr[size_t(p)],
+        sizeof(uint32_t) * size_t(P.contrib_ptr[size_t(p) + 1] - P.contrib_ptr[size_t(p)]));
+    blob.resize((blob.size() + 15) / 16 * 16, 0);
+    blob_off.push_back(int64_t(blob.size()));
+  }
   fo_status st = upload_vec(&m->d_plan.t_begin, P.t_begin);
   if (!st) st = upload_vec(&m->d_plan.col_ptr, P.col_ptr);
   if (!st) st = upload_vec(&m->d_plan.pair_ptr, P.pair_ptr);
-  if (!st) st = upload_vec(&m->d_plan.contrib_ptr, P.contrib_ptr);
-  if (!st) st = upload_vec(&m->d_plan.cols, P.cols);
-  if (!st) st = upload_vec(&m->d_plan.pairs, P.pairs);
-  if (!st) st = upload_vec(&m->d_plan.contrib, P.contrib);
+  if (!st) st = upload_vec(&m->d_plan.blob, blob);
+  if (!st) st = upload_vec(&m->d_plan.blob_off, blob_off);
   if (!st) st = upload_vec(&m->d_plan.zero_cols, P.zero_cols);
   if (!st) st = upload_vec(&m->d_plan.multi, P.multi);
   if (!st && P.n_partials > 0)
