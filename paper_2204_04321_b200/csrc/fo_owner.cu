@@ -122,32 +122,36 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
     double dg00 = 0.0, dg01 = 0.0, dg10 = 0.0, dg11 = 0.0;
     double up00 = 0.0, up01 = 0.0, up10 = 0.0, up11 = 0.0;
     double nx00 = 0.0, nx01 = 0.0, nx10 = 0.0, nx11 = 0.0;
-    const uint32_t* cp = sp.contrib + pp.off;
+    const uint32_t* cp = sp.contrib + pp.off;   // even count, 8-byte aligned
 #ifdef FO_EXPERIMENT_NO_GATHER
-    for (int e = 0; e < 0; ++e) {
+    for (int e = 0; e < 0; e += 2) {
 #else
-    for (int e = 0; e < pp.cnt; ++e) {
+    for (int e = 0; e < pp.cnt; e += 2) {
 #endif
-      const uint32_t cb = cp[e];
-      const int tl = int(cb & 255);
-      const int pat = int((cb >> 13) & 3);
-      const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
-      const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
-      dg00 += Dt[0];
-      dg01 += Dt[sb];
-      dg10 += Dt[sa];
-      dg11 += Dt[sa + sb];
-      if (UP) {
-        const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
-        const double* On = O + int((cb >> 20) & 31) * TP + tl;
-        up00 += Ou[0];
-        up01 += Ou[TP];
-        up10 += Ou[6 * TP];
-        up11 += Ou[7 * TP];
-        nx00 += On[0];
-        nx01 += On[6 * TP];
-        nx10 += On[TP];
-        nx11 += On[7 * TP];
+      const uint2 c2 = *reinterpret_cast<const uint2*>(cp + e);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t cb = h ? c2.y : c2.x;
+        const int tl = int(cb & 255);
+        const int pat = int((cb >> 13) & 3);
+        const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
+        const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
+        dg00 += Dt[0];
+        dg01 += Dt[sb];
+        dg10 += Dt[sa];
+        dg11 += Dt[sa + sb];
+        if (UP) {
+          const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
+          const double* On = O + int((cb >> 20) & 31) * TP + tl;
+          up00 += Ou[0];
+          up01 += Ou[TP];
+          up10 += Ou[6 * TP];
+          up11 += Ou[7 * TP];
+          nx00 += On[0];
+          nx01 += On[6 * TP];
+          nx10 += On[TP];
+          nx11 += On[7 * TP];
+        }
       }
     }
     const int nc = pc.info & 255;
@@ -184,11 +188,14 @@ __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, con
   for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
     const PlanCol& pc = sp.cols[ci];
     double r0 = 0.0, r1 = 0.0;
-    for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; ++e) {
-      const uint32_t cb = sp.contrib[e];
-      const double* Dr = D + (21 + 2 * int((cb >> 25) & 3)) * TP + int(cb & 255);
-      r0 += Dr[0];
-      r1 += Dr[TP];
+    for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; e += 2) {
+      const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + e);
+      const double* Da = D + (21 + 2 * int((c2.x >> 25) & 3)) * TP + int(c2.x & 255);
+      const double* Db = D + (21 + 2 * int((c2.y >> 25) & 3)) * TP + int(c2.y & 255);
+      r0 += Da[0];
+      r1 += Da[TP];
+      r0 += Db[0];
+      r1 += Db[TP];
     }
     if ((pc.info >> 30) & 1)
       *reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride + 12) =
@@ -316,6 +323,9 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
 #pragma unroll
     for (int i = 0; i < kD; ++i) D[i * TP + tl] = 0.0;
   }
+  // triangle slot kPatchTris: the zero column the plan's pad entries read
+  if (threadIdx.x < kD) D[threadIdx.x * TP + kPatchTris] = 0.0;
+  if (threadIdx.x < kO) O[threadIdx.x * TP + kPatchTris] = 0.0;
   for (int k = 0; k < L; ++k) {
     typename std::conditional<NEED_J, PatchSink, PatchSinkR>::type sk;
     sk.D = D;

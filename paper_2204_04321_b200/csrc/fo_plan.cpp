@@ -55,6 +55,7 @@ struct PatchBuild {
 //   bits 15-19  O index of (row (j,0), column (j2,0)) = 12 j + 2 j2
 //   bits 20-24  O index of (row (j2,0), column (j,0)) = 12 j2 + 2 j (transpose)
 //   bits 25-26  j (residual entry 21 + 2 j + a)
+// The code kPatchTris (tl = kPatchTris, all offsets 0) is the pad entry.
 uint32_t contrib_code(int tl, int j, int j2) {
   uint32_t dbase, pat;
   if (j == j2) { dbase = 12 + 3 * j; pat = 0; }
@@ -97,7 +98,10 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
     pc.info = int32_t(nc) | (interior ? 256 : 0) | (self << 9);
     const int32_t ci = int32_t(B.cols.size());
     for (int64_t s = 0; s < nc; ++s) {
-      const auto& l = per_slot[size_t(s)];
+      auto& l = per_slot[size_t(s)];
+      // even lengths: phase B gathers two contributions per step; the pad
+      // entry reads triangle slot kPatchTris, kept zero by the kernel
+      if (l.size() & 1) l.push_back(uint32_t(kPatchTris));
       if (s == self) {
         pc.self_off = uint16_t(B.contrib.size());
         pc.self_cnt = uint16_t(l.size());
