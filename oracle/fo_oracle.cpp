@@ -25,8 +25,12 @@
  *   6. scatter with plain += (no atomics), J entries located by binary search,
  *   Jacobian: the same residual code instantiated on Dual<12> (forward AD seeded
  *   on the wedge's 12 DOFs), the analogue of the paper's Sacado SFad.
+ *   NEXT-f1 (term ORA_LATERAL): lateral margin faces, P:133-140 / reading L12;
+ *   NEXT-f3 (T_star): A = A0 exp(-Q / (R T*)) per wedge.
  */
 #include "fo_oracle.h"
+
+#include <map>
 
 #include <algorithm>
 #include <cmath>
@@ -72,12 +76,15 @@ const double kTriXi[3] = {1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0};
 const double kTriEta[3] = {1.0 / 6.0, 1.0 / 6.0, 2.0 / 3.0};
 const double kTriW = 1.0 / 6.0;
 
+const double kGasR = 8.314462618;   /* J mol^-1 K^-1 (CODATA 2018) */
+
 struct Geo {           /* one wedge's data */
   double X[6][3];      /* nodal coordinates, local node i = t + 3*level */
   double s[6];         /* nodal surface elevation (of the node's column) */
   double beta[3];      /* basal friction at the 3 columns (after floating mask) */
   double A;            /* flow factor of this wedge */
   bool basal;          /* k == 0 */
+  int lateral;         /* bit jj: edge (jj, jj+1 mod 3) lies on the footprint boundary */
   int64_t gdof[12];    /* global DOFs, local dof = 2*i + a */
 };
 
@@ -207,6 +214,53 @@ void element(const Geo& e, const ora_params& p, int terms, const T Ul[12], T r[1
       energy += (0.5 * w * b) * (u * u + v * v);
     }
   }
+  if (terms & ORA_LATERAL) {
+    /* NEXT-f1: lateral margin faces, reading L12:
+     *   2 mu eps_a . n = [rho g (s - z) - rho_w g max(-z, 0)] n_a  on Gamma_l,
+     * so the weak form gains  - int_{Gamma_l} P(z) n_a phi_i dGamma.
+     * Quadrature (reading L20): 2-point Gauss along the edge; in zeta 2-point
+     * Gauss on [-1, 1], or on each side of the sea-level crossing z = 0. */
+    const double gz = 1.0 / std::sqrt(3.0);
+    for (int jj = 0; jj < 3; ++jj) {
+      if (!((e.lateral >> jj) & 1)) continue;
+      const int j0 = jj, j1 = (jj + 1) % 3;
+      const double dx = e.X[j1][0] - e.X[j0][0], dy = e.X[j1][1] - e.X[j0][1];
+      const double len = std::sqrt(dx * dx + dy * dy);
+      const double nx = dy / len, ny = -dx / len;     /* outward for a CCW triangle */
+      for (int sp = 0; sp < 2; ++sp) {
+        const double sc = 0.5 + (sp == 0 ? -0.5 : 0.5) * gz;   /* edge coordinate */
+        const double zb = (1.0 - sc) * e.X[j0][2] + sc * e.X[j1][2];
+        const double zt = (1.0 - sc) * e.X[j0 + 3][2] + sc * e.X[j1 + 3][2];
+        const double S = (1.0 - sc) * e.s[j0] + sc * e.s[j1];
+        double cut[3] = {-1.0, 1.0, 1.0};
+        int nint = 1;
+        if (zb < 0.0 && zt > 0.0) {
+          cut[1] = -1.0 + 2.0 * (0.0 - zb) / (zt - zb);
+          nint = 2;
+        }
+        for (int iv = 0; iv < nint; ++iv) {
+          const double lo = cut[iv], hi = cut[iv + 1];
+          for (int zq2 = 0; zq2 < 2; ++zq2) {
+            const double zeta = 0.5 * (lo + hi) + (zq2 == 0 ? -0.5 : 0.5) * (hi - lo) * gz;
+            const double wz = 0.5 * (hi - lo);
+            const double z = zb + 0.5 * (1.0 + zeta) * (zt - zb);
+            const double P = p.rho * p.g * (S - z) - p.rho_w * p.g * std::max(-z, 0.0);
+            const double W = len * 0.5 * wz * 0.5 * (zt - zb);
+            const double phi[4] = {(1.0 - sc) * 0.5 * (1.0 - zeta), sc * 0.5 * (1.0 - zeta),
+                                   (1.0 - sc) * 0.5 * (1.0 + zeta), sc * 0.5 * (1.0 + zeta)};
+            const int node[4] = {j0, j1, j0 + 3, j1 + 3};
+            T un = zero<T>();
+            for (int q = 0; q < 4; ++q) {
+              r[2 * node[q]] += promote<T>(-W * P * nx * phi[q]);
+              r[2 * node[q] + 1] += promote<T>(-W * P * ny * phi[q]);
+              un += (nx * phi[q]) * Ul[2 * node[q]] + (ny * phi[q]) * Ul[2 * node[q] + 1];
+            }
+            energy += (-W * P) * un;
+          }
+        }
+      }
+    }
+  }
   if (pi) *pi = energy;
 }
 
@@ -216,6 +270,7 @@ struct Mesh {
   int L;
   std::vector<double> z;      /* [n_node] */
   std::vector<double> beta;   /* masked */
+  std::vector<uint8_t> lateral;   /* [n_tri] boundary-edge bits (NEXT-f1) */
 };
 
 int validate(const ora_mesh* m) {
@@ -224,6 +279,7 @@ int validate(const ora_mesh* m) {
   if (m->n_vert == 0 && m->n_tri == 0) return 0;       /* empty footprint is valid */
   if (!m->xy || !m->tri || !m->thickness || !m->surface || !m->beta) return -1;
   if (m->p.glen_n <= 0.0 || m->p.A <= 0.0 || m->p.eps_reg < 0.0) return -1;
+  if (m->T_star && !(m->A0 > 0.0)) return -1;
   const int L = m->n_layers;
   if (m->sigma) {
     if (m->sigma[0] != 0.0 || m->sigma[L] != 1.0) return -2;
@@ -284,14 +340,35 @@ void wedge_geo(const Mesh& M, int64_t t, int k, Geo& e) {
       e.gdof[2 * i + 1] = 2 * node + 1;
     }
   for (int j = 0; j < 3; ++j) e.beta[j] = M.beta[v[j]];
-  e.A = m->A_elem ? m->A_elem[t * M.L + k] : m->p.A;
+  if (m->T_star)   /* Arrhenius relation */
+    e.A = m->A0 * std::exp(-m->Q_act / (kGasR * m->T_star[t * M.L + k]));
+  else
+    e.A = m->A_elem ? m->A_elem[t * M.L + k] : m->p.A;
   e.basal = (k == 0);
+  e.lateral = M.lateral.empty() ? 0 : M.lateral[t];
 }
 
-int prepare(const ora_mesh* m, Mesh& M) {
+/* footprint boundary edges: undirected edges used by exactly one triangle */
+void find_lateral(const ora_mesh* m, Mesh& M) {
+  std::map<std::pair<int32_t, int32_t>, int> cnt;
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int jj = 0; jj < 3; ++jj) {
+      int32_t a = m->tri[3 * t + jj], b = m->tri[3 * t + (jj + 1) % 3];
+      cnt[{std::min(a, b), std::max(a, b)}]++;
+    }
+  M.lateral.assign(m->n_tri, 0);
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int jj = 0; jj < 3; ++jj) {
+      int32_t a = m->tri[3 * t + jj], b = m->tri[3 * t + (jj + 1) % 3];
+      if (cnt[{std::min(a, b), std::max(a, b)}] == 1) M.lateral[t] |= uint8_t(1 << jj);
+    }
+}
+
+int prepare(const ora_mesh* m, Mesh& M, int terms = 0) {
   int st = validate(m);
   if (st) return st;
   extrude(m, M);
+  if (terms & ORA_LATERAL) find_lateral(m, M);
   return 0;
 }
 
@@ -335,7 +412,7 @@ int ora_graph(const ora_mesh* m, int64_t* row_ptr, int32_t* col_idx, int64_t* nn
 
 int ora_residual(const ora_mesh* m, int terms, const double* U, double* R, double* Mabs, double* Pi) {
   Mesh M;
-  int st = prepare(m, M);
+  int st = prepare(m, M, terms);
   if (st) return st;
   if (R) std::memset(R, 0, sizeof(double) * M.n_dof);
   if (Mabs) std::memset(Mabs, 0, sizeof(double) * M.n_dof);
@@ -360,7 +437,7 @@ int ora_residual(const ora_mesh* m, int terms, const double* U, double* R, doubl
 int ora_jacobian(const ora_mesh* m, int terms, const double* U, const int64_t* row_ptr,
                  const int32_t* col_idx, double* R, double* vals) {
   Mesh M;
-  int st = prepare(m, M);
+  int st = prepare(m, M, terms);
   if (st) return st;
   if (!row_ptr || !col_idx || !vals) return -1;
   if (R) std::memset(R, 0, sizeof(double) * M.n_dof);
@@ -392,7 +469,7 @@ int ora_jacobian(const ora_mesh* m, int terms, const double* U, const int64_t* r
 
 int ora_energy(const ora_mesh* m, int terms, const double* U, int64_t dof, double* Pi) {
   Mesh M;
-  int st = prepare(m, M);
+  int st = prepare(m, M, terms);
   if (st) return st;
   double total = 0.0;
   for (int64_t t = 0; t < m->n_tri; ++t)
@@ -414,7 +491,7 @@ int ora_energy(const ora_mesh* m, int terms, const double* U, int64_t dof, doubl
 int ora_element(const ora_mesh* m, int terms, const double* U, int64_t t, int32_t k,
                 double* r, double* Je, int64_t* gdof) {
   Mesh M;
-  int st = prepare(m, M);
+  int st = prepare(m, M, terms);
   if (st) return st;
   if (t < 0 || t >= m->n_tri || k < 0 || k >= M.L) return -1;
   Geo e;

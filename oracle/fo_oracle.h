@@ -15,6 +15,9 @@
  *   - the Newton Jacobian dF/dU (eq:linearsystem P:160-164) by fixed-size
  *     forward-mode AD (a Dual<12> number, the analogue of Sacado SFad);
  *   - the energy Pi whose gradient is F (reading R1-energy);
+ *   - NEXT-f1: the lateral margin term (ocean back-pressure, reading
+ *     L12, quadrature L20) on the boundary-edge faces, term ORA_LATERAL;
+ *   - NEXT-f3: the Arrhenius flow factor A = A0 exp(-Q/(R T*));
  *   - the CSR graph by brute force (std::set per row).
  * Readings where the paper is silent (quadrature, regularisation, basal measure,
  * floating mask, numbering) are listed in DESIGN.md section "Readings".
@@ -49,10 +52,17 @@ typedef struct {
   const double* beta;       /* [n_vert] */
   const double* A_elem;     /* [n_tri*L] or NULL */
   ora_params p;
+  /* NEXT-f3: A = A0 exp(-Q / (R T*)) per wedge when T_star != NULL
+   * (overrides A_elem and p.A); R = 8.314462618 J mol^-1 K^-1 */
+  const double* T_star;     /* [n_tri*L] K, or NULL */
+  double A0;                /* Pa^-n a^-1 */
+  double Q_act;             /* J mol^-1 */
 } ora_mesh;
 
 /* term mask for the pins: which integrals enter R / J / Pi */
-enum { ORA_VISC = 1, ORA_BODY = 2, ORA_BASAL = 4, ORA_ALL = 7 };
+enum { ORA_VISC = 1, ORA_BODY = 2, ORA_BASAL = 4, ORA_ALL = 7,
+       /* NEXT-f1: lateral margin term (reading L12), not in ORA_ALL */
+       ORA_LATERAL = 8 };
 
 /* validation (CCW, H >= H_min, sigma ascending 0..1, indices in range) */
 int ora_validate(const ora_mesh* m);

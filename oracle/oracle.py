@@ -17,7 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-VISC, BODY, BASAL, ALL = 1, 2, 4, 7
+VISC, BODY, BASAL, ALL, LATERAL = 1, 2, 4, 7, 8
 
 
 def build(force: bool = False) -> str:
@@ -40,7 +40,8 @@ class _Mesh(C.Structure):
     _fields_ = [("n_vert", C.c_int64), ("xy", C.c_void_p), ("n_tri", C.c_int64),
                 ("tri", C.c_void_p), ("n_layers", C.c_int32), ("sigma", C.c_void_p),
                 ("thickness", C.c_void_p), ("surface", C.c_void_p), ("bed", C.c_void_p),
-                ("beta", C.c_void_p), ("A_elem", C.c_void_p), ("p", _Params)]
+                ("beta", C.c_void_p), ("A_elem", C.c_void_p), ("p", _Params),
+                ("T_star", C.c_void_p), ("A0", C.c_double), ("Q_act", C.c_double)]
 
 
 _lib = None
@@ -89,6 +90,10 @@ class Oracle:
         self.beta = np.ascontiguousarray(fp.beta, dtype=np.float64)
         self.A_elem = None if getattr(fp, "A_elem", None) is None else \
             np.ascontiguousarray(fp.A_elem, dtype=np.float64)
+        # NEXT-f3: per-wedge temperature T* with the Arrhenius constants
+        self.T_star = None if getattr(fp, "T_star", None) is None else \
+            np.ascontiguousarray(fp.T_star, dtype=np.float64)
+        arr = getattr(fp, "arrhenius", None) or {}
         self.params = prm
         self.L = int(self.sigma.size - 1)
         self.n_vert = int(self.xy.shape[0])
@@ -98,7 +103,8 @@ class Oracle:
                         _ptr(self.sigma), _ptr(self.H), _ptr(self.s), _ptr(self.b),
                         _ptr(self.beta), _ptr(self.A_elem),
                         _Params(prm["rho"], prm["g"], prm["rho_w"], prm["glen_n"],
-                                prm["eps_reg"], prm["A"], prm["H_min"]))
+                                prm["eps_reg"], prm["A"], prm["H_min"]),
+                        _ptr(self.T_star), float(arr.get("A0", 0.0)), float(arr.get("Q", 0.0)))
         self._graph = None
 
     @property

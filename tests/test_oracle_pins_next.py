@@ -1,0 +1,160 @@
+"""Pins of the oracle's NEXT rows against closed forms and
+invariants, like tests/test_oracle_pins.py:
+  f1  lateral margin term (reading L12, quadrature L20),
+  f3  Arrhenius flow factor A = A0 exp(-Q / (R T*)).
+PAPER.md line citations: P:n.
+"""
+import numpy as np
+import pytest
+
+from paper_2204_04321_b200 import meshgen as mg
+
+RHO, G, RHO_W = 910.0, 9.81, 1028.0
+
+
+def _slab(H, s, nx=4, n_layers=3, seed=5):
+    fp = mg.slab(nx=nx, n_layers=n_layers, H0=H, seed=seed)
+    fp.surface = np.full(fp.n_vert, float(s))
+    return fp
+
+
+def _column_integral(H, s):
+    """int_{s-H}^{s} [rho g (s - z) - rho_w g max(-z, 0)] dz, written out."""
+    base = s - H
+    dry = RHO * G * H * H / 2.0
+    wet = 0.0
+    if base < 0.0:
+        top = min(s, 0.0)
+        wet = RHO_W * G * (base * base - top * top) / 2.0
+    return dry - wet
+
+
+# ---------------------------------------------------------------- f1
+@pytest.mark.parametrize("case", ["floating", "grounded-cliff", "partly-submerged"])
+def test_f1_lateral_side_totals(ora_mod, case):
+    """Sum of the lateral residual over the nodes of one straight side of a
+    uniform slab = -(side length) n_a int P dz (the depth-integrated margin
+    force; for the floating front 1/2 rho g H^2 (1 - rho/rho_w), L12)."""
+    H = 1000.0
+    s = {"floating": H * (1.0 - RHO / RHO_W), "grounded-cliff": 1500.0,
+         "partly-submerged": 700.0}[case]
+    fp = _slab(H, s)
+    o = ora_mod.Oracle(fp)
+    R = o.residual(np.zeros(o.n_dof), terms=ora_mod.LATERAL)[0].reshape(fp.n_vert, fp.n_layers + 1, 2)
+    x, y = fp.xy[:, 0], fp.xy[:, 1]
+    Lx = x.max() - x.min()
+    Ly = y.max() - y.min()
+    I = _column_integral(H, s)
+    if case == "floating":
+        assert I == pytest.approx(0.5 * RHO * G * H * H * (1.0 - RHO / RHO_W), rel=1e-12)
+    scale = Ly * abs(I)
+    assert abs(R[x == x.max(), :, 0].sum() - (-Ly * I)) <= 1e-12 * scale
+    assert abs(R[x == x.min(), :, 0].sum() - (+Ly * I)) <= 1e-12 * scale
+    assert abs(R[y == y.max(), :, 1].sum() - (-Lx * I)) <= 1e-12 * scale
+    assert abs(R[y == y.min(), :, 1].sum() - (+Lx * I)) <= 1e-12 * scale
+    # only margin columns are touched
+    inner = (x > x.min()) & (x < x.max()) & (y > y.min()) & (y < y.max())
+    assert np.abs(R[inner]).max() == 0.0
+
+
+def test_f1_lateral_per_face_levels(ora_mod):
+    """On a uniform grounded slab (no water) the level split of one side's
+    force is the P1-in-z integral of the linear pressure: for a layer [z0, z1]
+    the bottom node gets int P (z1 - z)/(z1 - z0) dz; summed along the side."""
+    H, s = 800.0, 2000.0
+    fp = _slab(H, s, n_layers=4)
+    o = ora_mod.Oracle(fp)
+    R = o.residual(np.zeros(o.n_dof), terms=ora_mod.LATERAL)[0].reshape(fp.n_vert, fp.n_layers + 1, 2)
+    x, y = fp.xy[:, 0], fp.xy[:, 1]
+    Ly = y.max() - y.min()
+    z = (s - H) + fp.sigma * H
+    expect = np.zeros(fp.n_layers + 1)
+    for k in range(fp.n_layers):
+        z0, z1 = z[k], z[k + 1]
+        h = z1 - z0
+        # P(z) = rho g (s - z); int_z0^z1 P (z1-z)/h dz and int P (z-z0)/h dz (closed form)
+        p0, p1 = RHO * G * (s - z0), RHO * G * (s - z1)
+        expect[k] += h * (2 * p0 + p1) / 6.0
+        expect[k + 1] += h * (p0 + 2 * p1) / 6.0
+    got = R[x == x.max(), :, 0].sum(axis=0)
+    assert np.abs(got - (-Ly * expect)).max() <= 1e-12 * Ly * expect.max()
+
+
+def test_f1_lateral_is_energy_gradient(ora_mod):
+    """R = grad Pi with the lateral term included (P12 extended): the margin
+    work term is linear in U."""
+    fp = mg.greenland_like(80.0, n_layers=3)
+    o = ora_mod.Oracle(fp)
+    terms = ora_mod.ALL | ora_mod.LATERAL
+    U = fp.U
+    R = o.residual(U, terms=terms)[0]
+    Rl = o.residual(U, terms=ora_mod.LATERAL)[0]
+    assert np.abs(Rl).max() > 0.0
+    margin = np.nonzero(Rl)[0]
+    for j in list(margin[:: max(1, margin.size // 12)]) + [0, o.n_dof // 2]:
+        h = 1e-4 * max(1.0, abs(U[j]))
+        Up, Um = U.copy(), U.copy()
+        Up[j] += h
+        Um[j] -= h
+        fd = (o.energy(Up, dof=j, terms=terms) - o.energy(Um, dof=j, terms=terms)) / (2 * h)
+        assert abs(fd - R[j]) <= 1e-6 * np.abs(R).max(), (j, fd, R[j])
+
+
+def test_f1_lateral_leaves_jacobian_unchanged(ora_mod):
+    fp = mg.ismip_hom_a(nx=4, n_layers=2)
+    o = ora_mod.Oracle(fp)
+    _, v1 = o.jacobian(fp.U)
+    _, v2 = o.jacobian(fp.U, terms=ora_mod.ALL | ora_mod.LATERAL)
+    assert np.array_equal(v1, v2)
+
+
+# ---------------------------------------------------------------- f3
+def _with_temperature(fp, T, A0, Q):
+    fp.T_star = np.asarray(T, dtype=np.float64)
+    fp.arrhenius = dict(A0=A0, Q=Q)
+    return fp
+
+
+def test_f3_zero_activation_energy_is_constant_A(ora_mod):
+    """Q = 0: A = A0 for any T*, the scalar-A path exactly."""
+    fp = mg.ismip_hom_a(nx=4, n_layers=3)
+    A0 = 2.5e-16
+    ref = ora_mod.Oracle(fp, params=dict(A=A0))
+    T = 240.0 + 30.0 * mg.SplitMix64(3).uniform(fp.n_elem)
+    fp2 = _with_temperature(mg.ismip_hom_a(nx=4, n_layers=3), T, A0, 0.0)
+    o = ora_mod.Oracle(fp2)
+    assert np.array_equal(o.residual(fp.U)[0], ref.residual(fp.U)[0])
+    assert np.array_equal(o.jacobian(fp.U)[1], ref.jacobian(fp.U)[1])
+
+
+def test_f3_arrhenius_temperature_ratio(ora_mod):
+    """Uniform T*: the viscous residual scales as A^(-1/n) (flow-law
+    homogeneity in A), so R(T1) / R(T2) = exp(Q/(n R) (1/T1 - 1/T2))."""
+    Rgas, Q, A0 = 8.314462618, 6.0e4, 1.0e-3
+    out = {}
+    for T in (250.0, 265.0):
+        fp = _with_temperature(mg.ismip_hom_a(nx=4, n_layers=3), np.full(4 * 4 * 2 * 3, T), A0, Q)
+        out[T] = ora_mod.Oracle(fp).residual(fp.U, terms=ora_mod.VISC)[0]
+    ratio = np.exp(Q / (3.0 * Rgas) * (1.0 / 250.0 - 1.0 / 265.0))
+    assert np.abs(out[250.0] - ratio * out[265.0]).max() <= 1e-13 * np.abs(out[250.0]).max()
+
+
+def test_f3_temperature_is_per_wedge(ora_mod):
+    """Changing T* of one wedge changes only the residual rows of its 12 DOFs."""
+    fp = mg.ismip_hom_a(nx=4, n_layers=3)
+    T = np.full(fp.n_elem, 255.0)
+    o1 = ora_mod.Oracle(_with_temperature(fp, T, 1e-3, 6e4))
+    R1 = o1.residual(fp.U)[0]
+    w = 17
+    T2 = T.copy()
+    T2[w] = 268.0
+    fp2 = _with_temperature(mg.ismip_hom_a(nx=4, n_layers=3), T2, 1e-3, 6e4)
+    R2 = ora_mod.Oracle(fp2).residual(fp.U)[0]
+    t, k = divmod(w, fp.n_layers)
+    dofs = set()
+    for j in range(3):
+        for lev in (k, k + 1):
+            node = int(fp.tri[t][j]) * (fp.n_layers + 1) + lev
+            dofs.update((2 * node, 2 * node + 1))
+    changed = set(np.nonzero(R1 != R2)[0].tolist())
+    assert changed and changed <= dofs
