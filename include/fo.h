@@ -110,6 +110,16 @@ FO_API fo_status fo_mesh_create_part(const fo_params* p, int64_t n_vert, const d
                               const int32_t* part_of_tri, int32_t my_part,
                               int32_t n_parts, int device, fo_mesh* out);
 
+/* NEXT-f3: temperature-dependent flow factor
+ *   A = A0 exp(-Q / (R T*)),  R = 8.314462618 J mol^-1 K^-1,
+ * per wedge, evaluated inside the assembly kernels (8 bytes of T* per wedge;
+ * DESIGN.md reading L21).  T_star[n_tri*L] (K, pressure-corrected, wedge
+ * t*L+k of the GLOBAL footprint for a part mesh) is copied to the device
+ * (the caller may free it on return); A0 in Pa^-n a^-1, Q in J mol^-1.
+ * Replaces p->A / A_elem for later assemblies; T_star == NULL reverts to them.
+ * FO_EINVAL: mesh NULL, A0 <= 0 or some T* <= 0.  Synchronous. */
+FO_API fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, double Q);
+
 /* Contiguous partition of the (Hilbert-ordered) triangle list:
  * part_of_tri[t] = floor(t * n_parts / n_tri).  Host only. */
 FO_API fo_status fo_partition(int64_t n_tri, int32_t n_parts, int32_t* part_of_tri);
@@ -152,6 +162,15 @@ FO_API fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, 
  * copy bandwidth.  h_R may be NULL. */
 FO_API fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, double* h_R,
                                     double* h_vals, void* stream);
+
+/* NEXT-f1: lateral margin term of the residual on the footprint
+ * boundary faces (boundary edges of the GLOBAL footprint x L layers), by
+ * DESIGN.md reading L12:  2 mu eps_a . n = [rho g (s - z) - rho_w g max(-z, 0)] n_a,
+ * i.e.  R_{a,i} -= int_{Gamma_l} P(z) n_a phi_i dGamma  (quadrature: reading L20).
+ * U-independent: the Jacobian values are unchanged.  enable = 0 (default)
+ * leaves it out.  Applies to later fo_assemble_* calls on this mesh (one extra
+ * kernel, one writer per residual entry: deterministic). */
+FO_API fo_status fo_set_lateral(fo_mesh m, int enable);
 
 /* Scatter strategy of fo_assemble_jacobian (ablation; default FO_SCATTER_OWNER):
  * FO_SCATTER_OWNER  column-patch owner-computes kernel: every CSR value written

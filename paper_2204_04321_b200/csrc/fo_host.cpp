@@ -349,6 +349,7 @@ fo_status mesh_create_impl(const fo_params* p, int64_t n_vert, const double* xy,
     m->has_A_elem = true;
   }
   if (!st) st = build_patch_plan(m);
+  if (!st) st = build_lateral(m, n_tri, tri);
   if (st) { fo_mesh_destroy(m); return st; }
   *out = m;
   return FO_OK;
@@ -362,6 +363,32 @@ using namespace fo;
 extern "C" {
 
 const char* fo_last_error(void) { return g_err.c_str(); }
+
+fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, double Q) {
+  if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (m->d_T) cudaSetDevice(m->device);
+  cudaFree(m->d_T);
+  m->d_T = nullptr;
+  if (!T_star) return FO_OK;
+  if (!(A0 > 0.0)) return fail(FO_EINVAL, "A0 must be > 0");
+  constexpr double kGasR = 8.314462618;   // J mol^-1 K^-1 (CODATA 2018)
+  const int32_t L = m->L;
+  std::vector<double> T(size_t(m->n_elem));
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int32_t k = 0; k < L; ++k) {
+      const double v = T_star[m->tri_glob[size_t(t)] * L + k];
+      if (!(v > 0.0)) return fail(FO_EINVAL, "T_star must be > 0 K");
+      T[size_t(t * L + k)] = v;
+    }
+  m->A0fac = std::pow(A0, -1.0 / m->p.glen_n);
+  m->QnR = Q / (m->p.glen_n * kGasR);
+  if (T.empty()) return FO_OK;
+  cudaSetDevice(m->device);
+  fo_status st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_T), T.size() * sizeof(double)), "cudaMalloc");
+  if (!st) st = cuda_status(cudaMemcpy(m->d_T, T.data(), T.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
+  if (st) { cudaFree(m->d_T); m->d_T = nullptr; }
+  return st;
+}
 
 fo_status fo_params_default(fo_params* p) {
   if (!p) return fail(FO_EINVAL, "params is NULL");
@@ -539,6 +566,12 @@ fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, do
   return st;
 }
 
+fo_status fo_set_lateral(fo_mesh m, int enable) {
+  if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  m->lateral = enable != 0;
+  return FO_OK;
+}
+
 fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
   if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC) return fail(FO_EINVAL, "bad scatter");
@@ -584,6 +617,10 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_tri);
   cudaFree(m->d_sigma);
   cudaFree(m->d_A);
+  cudaFree(m->d_T);
+  cudaFree(m->d_lat_cols);
+  cudaFree(m->d_lat_faces);
+  cudaFree(m->d_lat_refs);
   cudaFree(m->d_plan.t_begin);
   cudaFree(m->d_plan.col_ptr);
   cudaFree(m->d_plan.pair_ptr);

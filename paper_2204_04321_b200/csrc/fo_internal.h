@@ -2,6 +2,7 @@
 // Layout and numbering: DESIGN.md "Layout in HBM"; public contract: include/fo.h.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 #include <string>
 #include <vector>
 
@@ -129,6 +130,14 @@ struct fo_mesh_s {
   fo::TriRec* d_tri = nullptr;
   double* d_sigma = nullptr;
   double* d_A = nullptr;           // per-wedge A^(-1/n) or nullptr
+  double* d_T = nullptr;           // per-wedge T* (NEXT-f3) or nullptr
+  double A0fac = 0.0, QnR = 0.0;   // Arrhenius constants folded for the kernels
+  // NEXT-f1 lateral margin term (fo_lateral.cu)
+  bool lateral = false;
+  int32_t n_lat_cols = 0, n_lat_faces = 0;
+  int4* d_lat_cols = nullptr;      // (column, first ref, ref count, 0)
+  int2* d_lat_faces = nullptr;     // (c0, c1) CCW edge of a margin face
+  int32_t* d_lat_refs = nullptr;   // face * 2 + role
   fo::PatchPlan plan;
   fo::DevPatch d_plan;
   fo_scatter scatter = FO_SCATTER_OWNER;
@@ -173,4 +182,7 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
 fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_vals,
                           void* stream);
 fo_status build_patch_plan(fo_mesh m);
+// NEXT-f1 lateral margin term (fo_lateral.cu)
+fo_status build_lateral(fo_mesh m, int64_t n_tri_global, const int32_t* tri_global);
+fo_status launch_lateral(fo_mesh m, double* d_R, void* stream);
 }  // namespace fo

@@ -88,13 +88,14 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
-    return launch_owner(m, d_U, d_R, nullptr, s);
+    st = launch_owner(m, d_U, d_R, nullptr, s);
+  } else {
+    st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
+    if (st || m->n_elem == 0) return st;
+    st = launch_atomic<false>(m, d_U, d_R, nullptr, s);
+    m->last_launches = 1;
   }
-  st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
-  if (st) return st;
-  if (m->n_elem == 0) return FO_OK;
-  st = launch_atomic<false>(m, d_U, d_R, nullptr, s);
-  m->last_launches = 1;
+  if (!st) st = launch_lateral(m, d_R, s);
   return st;
 }
 
@@ -106,15 +107,16 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
-    return launch_owner(m, d_U, d_R, d_vals, s);
+    st = launch_owner(m, d_U, d_R, d_vals, s);
+  } else {
+    if (d_R) st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
+    if (!st && m->nnz > 0)
+      st = cuda_status(cudaMemsetAsync(d_vals, 0, sizeof(double) * m->nnz, s), "cudaMemsetAsync");
+    if (st || m->n_elem == 0) return st;
+    st = launch_atomic<true>(m, d_U, d_R, d_vals, s);
+    m->last_launches = 1;
   }
-  if (d_R) st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
-  if (!st && m->nnz > 0)
-    st = cuda_status(cudaMemsetAsync(d_vals, 0, sizeof(double) * m->nnz, s), "cudaMemsetAsync");
-  if (st) return st;
-  if (m->n_elem == 0) return FO_OK;
-  st = launch_atomic<true>(m, d_U, d_R, d_vals, s);
-  m->last_launches = 1;
+  if (!st) st = launch_lateral(m, d_R, s);
   return st;
 }
 

@@ -16,6 +16,10 @@ struct KParams {
   double glen_n;      // n
   double Afac;        // A^(-1/n) when no per-wedge field
   int go;             // 1 (opaque to the compiler)
+  // NEXT-f3: per-wedge T* -> A^(-1/n) = A0^(-1/n) exp(Q / (n R T*))
+  const double* Tw;   // [n_elem] or nullptr
+  double A0fac;       // A0^(-1/n)
+  double QnR;         // Q / (n R)
 };
 
 inline KParams make_kparams(fo_mesh m) {
@@ -27,7 +31,19 @@ inline KParams make_kparams(fo_mesh m) {
   kp.glen_n = m->p.glen_n;
   kp.Afac = pow(m->p.A, -1.0 / m->p.glen_n);
   kp.go = 1;
+  kp.Tw = m->d_T;
+  kp.A0fac = m->A0fac;
+  kp.QnR = m->QnR;
   return kp;
+}
+
+// A^(-1/n) of wedge (t, k): Arrhenius from T* (NEXT-f3), else the per-wedge
+// field, else the scalar (fused into the viscosity step a5)
+__device__ __forceinline__ double wedge_afac(const KParams& kp, const double* __restrict__ Aw,
+                                             int64_t t, int k) {
+  const int64_t w = t * kp.L + k;
+  if (kp.Tw) return kp.A0fac * exp(kp.QnR / __ldg(kp.Tw + w));
+  return Aw ? __ldg(Aw + w) : kp.Afac;
 }
 
 // Per-triangle geometry (layer independent): barycentric gradients, 2|T|,
@@ -111,7 +127,7 @@ __device__ __forceinline__ void load_wedge(const ColRec* __restrict__ col,
   load_tri_geo(col, tr, g);
 #pragma unroll
   for (int j = 0; j < 3; ++j) cr[j].cs_n = (g.cs[j] << 8) | g.nc[j];
-  const double Afac = Aw ? __ldg(Aw + t * kp.L + k) : kp.Afac;
+  const double Afac = wedge_afac(kp, Aw, t, k);
   wedge_input(g, tr, sigma, Afac, U, kp.L, k, w);
 }
 

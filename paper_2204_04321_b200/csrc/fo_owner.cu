@@ -338,7 +338,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       asm volatile("" : "+l"(colk));
       TriGeo geo;
       load_tri_geo(colk, tr, geo);
-      const double Afac = Aw ? __ldg(Aw + int64_t(t0 + tl) * L + k) : kp.Afac;
+      const double Afac = wedge_afac(kp, Aw, t0 + tl, k);
       WedgeIn w;
       wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
       SmemCmp cmp{C, tl};

@@ -59,6 +59,8 @@ _SIGS = {
     "fo_assemble_jacobian": [P, P, P, P, P, P],
     "fo_assemble_jacobian_host": [P, P, P, P, P, P],
     "fo_set_scatter": [P, C.c_int],
+    "fo_mesh_set_temperature": [P, P, C.c_double, C.c_double],
+    "fo_set_lateral": [P, C.c_int],
     "fo_last_launch_count": [P, P],
     "fo_kernel_timing": [P, I32],
     "fo_kernel_time_ms": [P, P, P],
@@ -325,6 +327,20 @@ class Mesh:
         if self._graph is None:
             self._graph = Graph(self)
         return self._graph
+
+    def set_temperature(self, T_star, A0: float = 0.0, Q: float = 0.0):
+        """NEXT-f3: A = A0 exp(-Q / (R T*)) per wedge; T_star is a
+        host array [n_tri*L] of the (global) footprint, None reverts."""
+        if T_star is None:
+            check(lib().fo_mesh_set_temperature(self.handle, None, 0.0, 0.0), "fo_mesh_set_temperature")
+            return
+        T = np.ascontiguousarray(T_star, dtype=np.float64)
+        check(lib().fo_mesh_set_temperature(self.handle, T.ctypes.data, float(A0), float(Q)),
+              "fo_mesh_set_temperature")
+
+    def set_lateral(self, on: bool = True):
+        """NEXT-f1: include the lateral margin term in R."""
+        check(lib().fo_set_lateral(self.handle, 1 if on else 0), "fo_set_lateral")
 
     def set_scatter(self, mode: int):
         check(lib().fo_set_scatter(self.handle, int(mode)), "fo_set_scatter")

@@ -83,6 +83,8 @@ class Footprint:
     U: np.ndarray           # float64 [2*n_vert*(L+1)]
     params: dict
     A_elem: np.ndarray | None = None
+    T_star: np.ndarray | None = None    # NEXT-f3: per-wedge temperature (K)
+    arrhenius: dict | None = None       # {"A0": Pa^-n a^-1, "Q": J/mol}
 
     @property
     def n_vert(self) -> int:
@@ -512,7 +514,9 @@ def sub_footprint(fp: Footprint, t0: int, t1: int) -> Footprint:
                      remap[tri].astype(np.int32), fp.sigma.copy(), fp.thickness[verts].copy(),
                      fp.surface[verts].copy(), None if fp.bed is None else fp.bed[verts].copy(),
                      fp.beta[verts].copy(), Uv, dict(fp.params),
-                     None if fp.A_elem is None else fp.A_elem.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy())
+                     None if fp.A_elem is None else fp.A_elem.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy(),
+                     None if fp.T_star is None else fp.T_star.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy(),
+                     None if fp.arrhenius is None else dict(fp.arrhenius))
 
 
 def sub_footprint_tris(fp: Footprint, tri_ids) -> Footprint:
@@ -529,9 +533,29 @@ def sub_footprint_tris(fp: Footprint, tri_ids) -> Footprint:
     sub = Footprint(fp.name + "[subset]", fp.xy[verts].copy(), remap[tri].astype(np.int32),
                     fp.sigma.copy(), fp.thickness[verts].copy(), fp.surface[verts].copy(),
                     None if fp.bed is None else fp.bed[verts].copy(), fp.beta[verts].copy(), Uv,
-                    dict(fp.params), A)
+                    dict(fp.params), A,
+                    None if fp.T_star is None else fp.T_star.reshape(fp.n_tri, -1)[tri_ids].reshape(-1).copy(),
+                    None if fp.arrhenius is None else dict(fp.arrhenius))
     sub.vertex_ids = verts
     return sub
+
+
+# Arrhenius constants of the synthetic temperature recipe (cold-ice branch of
+# the Paterson-Budd fit, converted to years): A0 = 3.61e-13 Pa^-3 s^-1, Q = 60 kJ/mol
+ARRHENIUS_COLD = dict(A0=3.61e-13 * 31556926.0, Q=6.0e4)
+
+
+def with_temperature(fp: Footprint, seed: int = 7, T_surf: float = 243.0,
+                     T_bed: float = 268.0, noise: float = 2.0) -> Footprint:
+    """NEXT-f3 input recipe: per-wedge T* linear in the mid-layer sigma,
+    T_surf at the surface to T_bed at the bed, plus seeded noise (+-noise K);
+    sets fp.T_star and fp.arrhenius in place and returns fp."""
+    rng = SplitMix64(seed)
+    sm = 0.5 * (fp.sigma[:-1] + fp.sigma[1:])
+    T = (T_bed + (T_surf - T_bed) * sm)[None, :] + noise * (2.0 * rng.uniform(fp.n_elem).reshape(fp.n_tri, -1) - 1.0)
+    fp.T_star = T.reshape(-1)
+    fp.arrhenius = dict(ARRHENIUS_COLD)
+    return fp
 
 
 def by_name(name: str) -> Footprint:

@@ -24,11 +24,15 @@ def torch_cuda():
     return torch
 
 
-def gpu_assemble(torch, fp, params=None, scatter=None):
+def gpu_assemble(torch, fp, params=None, scatter=None, lateral=False):
     from paper_2204_04321_b200 import fo
     mesh = fo.Mesh.from_footprint(fp, params=params)
+    if lateral:
+        mesh.set_lateral(True)
     if scatter is not None:
         mesh.set_scatter(scatter)
+    if getattr(fp, "T_star", None) is not None:
+        mesh.set_temperature(fp.T_star, fp.arrhenius["A0"], fp.arrhenius["Q"])
     U = torch.tensor(fp.U, dtype=torch.float64, device="cuda")
     R = mesh.residual(U)
     RJ, vals = mesh.jacobian(U)
@@ -39,12 +43,13 @@ def gpu_assemble(torch, fp, params=None, scatter=None):
     return out
 
 
-def check_parity(o, g, params=None, fp=None):
-    R, M, _ = o.residual(fp.U)
+def check_parity(o, g, params=None, fp=None, terms=None):
+    kw = {} if terms is None else dict(terms=terms)
+    R, M, _ = o.residual(fp.U, **kw)
     rp, col = o.graph()
     assert g["row_ptr"].tobytes() == rp.tobytes()
     assert g["col"].tobytes() == col.tobytes()
-    _, vals = o.jacobian(fp.U)
+    _, vals = o.jacobian(fp.U, **kw)
     scale = np.abs(M).max() if M.size else 1.0
     assert np.abs(g["R"] - R).max(initial=0.0) <= R_TOL * scale
     assert np.abs(g["RJ"] - R).max(initial=0.0) <= R_TOL * scale
@@ -96,6 +101,50 @@ def test_parity_A_elem_and_floating(torch_cuda, ora_mod):
     assert (fp.params["rho"] * fp.thickness < -fp.params["rho_w"] * fp.bed).any()
     g = gpu_assemble(torch_cuda, fp)
     check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_parity_temperature_flow_factor(torch_cuda, ora_mod, scatter):
+    """NEXT-f3: A = A0 exp(-Q/(R T*)) per wedge inside the kernels."""
+    fp = mg.with_temperature(mg.greenland_like(60.0, n_layers=6))
+    g = gpu_assemble(torch_cuda, fp, scatter=scatter)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+    # reverting restores the scalar-A assembly
+    fp0 = mg.greenland_like(60.0, n_layers=6)
+    g0 = gpu_assemble(torch_cuda, fp0, scatter=scatter)
+    g["mesh"].set_temperature(None)
+    import torch
+    R = g["mesh"].residual(torch.tensor(fp.U, device="cuda")).cpu().numpy()
+    if scatter == 0:   # owner-computes: bitwise reproducible
+        assert np.array_equal(R, g0["R"])
+    else:              # atomic ablation: summation order varies
+        assert np.abs(R - g0["R"]).max() <= 1e-13 * np.abs(g0["R"]).max()
+
+
+@pytest.mark.parametrize("scatter", SCATTERS)
+@pytest.mark.parametrize("case", ["gris-60km", "C5-small"])
+def test_parity_lateral_margin_term(torch_cuda, ora_mod, case, scatter):
+    """NEXT-f1: lateral margin term (readings L12/L20); C5-small has
+    floating fronts (water pressure below sea level)."""
+    if case == "C5-small":
+        fp = mg.antarctica_like(D_km=150.0, n_layers=3)
+        fp = mg.sub_footprint(fp, 0, min(fp.n_tri, 6000))
+    else:
+        fp = mg.greenland_like(60.0, n_layers=6)
+    g = gpu_assemble(torch_cuda, fp, scatter=scatter, lateral=True)
+    o = ora_mod.Oracle(fp)
+    check_parity(o, g, fp=fp, terms=ora_mod.ALL | ora_mod.LATERAL)
+    # the lateral term alone, at a scale where it is not hidden by the viscous
+    # part: at U = 0 only the driving stress and the margin term remain
+    import torch
+    U0 = torch.zeros(fp.n_dof, dtype=torch.float64, device="cuda")
+    R_on = g["mesh"].residual(U0).cpu().numpy()
+    g["mesh"].set_lateral(False)
+    R_off = g["mesh"].residual(U0).cpu().numpy()
+    Rl = o.residual(np.zeros(fp.n_dof), terms=ora_mod.LATERAL)[0]
+    Rb, Mb, _ = o.residual(np.zeros(fp.n_dof), terms=ora_mod.BODY | ora_mod.LATERAL)
+    assert np.abs(Rl).max() > 0.0
+    assert np.abs((R_on - R_off) - Rl).max() <= R_TOL * np.abs(Mb).max()
 
 
 @pytest.mark.parametrize("L", [1, 2, 17])
@@ -201,8 +250,9 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod):
                 assert np.abs(seg_g - seg_o).max() <= J_TOL * np.abs(seg_o).max()
 
 
+@pytest.mark.parametrize("lateral", [False, True])
 @pytest.mark.parametrize("P", [2, 3])
-def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P):
+def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P, lateral):
     """local meshes of a P-way footprint partition (fo_mesh_create_part) on one
     GPU, ghost-row partial sums added into the owners with the library's halo
     plan (the data movement fo_halo_sum does over NCCL): owned rows equal the
@@ -213,12 +263,14 @@ def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P):
     L = fp.n_layers
     part = fo.partition(fp.n_tri, P)
     full = fo.Mesh.from_footprint(fp)
+    full.set_lateral(lateral)
     Rf, Vf = full.jacobian(torch.tensor(fp.U, device="cuda"))
     grp, gcol = full.graph().to_host()
     Rf, Vf = Rf.cpu().numpy(), Vf.cpu().numpy()
     meshes, outs = [], []
     for p in range(P):
         m = fo.Mesh.from_footprint(fp, part=part, my_part=p, n_parts=P)
+        m.set_lateral(lateral)
         glob, nA, nB, nC = m.columns()
         Ul = fp.U.reshape(fp.n_vert, L + 1, 2)[glob].reshape(-1)
         R, V = m.jacobian(torch.tensor(Ul, device="cuda"))
@@ -252,7 +304,8 @@ def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P):
 
 def test_c3_bitwise_reproducible_and_overwritten(torch_cuda):
     """the owner-computes scatter is bitwise run-to-run
-    stable (lead-patch stores, then adds in patch order), and every output
+    stable (interior stores; at most two RED partial sums per boundary entry;
+    sums of three or more patches added in patch order), and every output
     entry is overwritten (NaN-filled buffers come back NaN-free)."""
     import torch
     from paper_2204_04321_b200 import fo
