@@ -163,6 +163,33 @@ FO_API fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, 
 FO_API fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, double* h_R,
                                     double* h_vals, void* stream);
 
+/* ---- NEXT-f2: the Newton consumer of the assembled Jacobian ----
+ * Single-domain meshes only (FO_ESTATE for a part mesh).  All buffers are
+ * caller-owned contiguous fp64 device arrays of n_dofs entries unless stated;
+ * work is enqueued on `stream`, no host synchronisation.
+ *
+ * y = J x, J the CSR values d_vals of fo_assemble_jacobian for graph g.  Every
+ * value position comes from the column structure (row (c,k,a) couples slot s
+ * of c's sorted neighbour list, levels k-1..k+1, comps 0..1), so col_idx is
+ * never read.  One writer per y entry (deterministic). */
+FO_API fo_status fo_spmv(fo_mesh m, fo_graph g, const double* d_vals, const double* d_x, double* d_y,
+                         void* stream);
+/* Vertical-line preconditioner: factor, for every column, the 2x2-block
+ * tridiagonal block of J coupling the column's own 2(L+1) DOFs (block Thomas;
+ * factors kept in the mesh; d_vals must stay valid until the next factor).
+ * fo_line_solve: z = M^-1 r with M = those column blocks (block Jacobi over
+ * vertical lines).  FO_ESTATE if fo_line_factor was not called. */
+FO_API fo_status fo_line_factor(fo_mesh m, fo_graph g, const double* d_vals, void* stream);
+FO_API fo_status fo_line_solve(fo_mesh m, const double* d_r, double* d_z, void* stream);
+/* Krylov helpers on the mesh's device (fixed-order reductions, bitwise
+ * reproducible): d_out[j] = V_j . w for j < k (1 <= k <= 64), and
+ * w -= sum_j h_j V_j (h: k doubles on the device).  V column-major, column j at
+ * d_V + j * ldv, ldv >= n. */
+FO_API fo_status fo_krylov_dots(fo_mesh m, int64_t n, int32_t k, const double* d_V, int64_t ldv,
+                                const double* d_w, double* d_out, void* stream);
+FO_API fo_status fo_krylov_update(fo_mesh m, int64_t n, int32_t k, const double* d_V, int64_t ldv,
+                                  const double* d_h, double* d_w, void* stream);
+
 /* NEXT-f1: lateral margin term of the residual on the footprint
  * boundary faces (boundary edges of the GLOBAL footprint x L layers), by
  * DESIGN.md reading L12:  2 mu eps_a . n = [rho g (s - z) - rho_w g max(-z, 0)] n_a,

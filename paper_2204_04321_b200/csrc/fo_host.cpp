@@ -621,6 +621,11 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_lat_cols);
   cudaFree(m->d_lat_faces);
   cudaFree(m->d_lat_refs);
+  cudaFree(m->d_nbr_ptr);
+  cudaFree(m->d_nbr);
+  cudaFree(m->d_self_slot);
+  cudaFree(m->d_line_fac);
+  cudaFree(m->d_kry_work);
   cudaFree(m->d_plan.t_begin);
   cudaFree(m->d_plan.col_ptr);
   cudaFree(m->d_plan.pair_ptr);

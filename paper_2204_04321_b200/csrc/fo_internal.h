@@ -138,6 +138,13 @@ struct fo_mesh_s {
   int4* d_lat_cols = nullptr;      // (column, first ref, ref count, 0)
   int2* d_lat_faces = nullptr;     // (c0, c1) CCW edge of a margin face
   int32_t* d_lat_refs = nullptr;   // face * 2 + role
+  // NEXT-f2 Newton consumer (fo_solve.cu), allocated on first use
+  int64_t* d_nbr_ptr = nullptr;
+  int32_t* d_nbr = nullptr;
+  int32_t* d_self_slot = nullptr;
+  double* d_line_fac = nullptr;    // [n_cols][L+1][8] block Thomas factors
+  double* d_kry_work = nullptr;    // dot-product partials
+  const double* line_vals = nullptr;   // the values fo_line_factor factored
   fo::PatchPlan plan;
   fo::DevPatch d_plan;
   fo_scatter scatter = FO_SCATTER_OWNER;

@@ -61,6 +61,11 @@ _SIGS = {
     "fo_set_scatter": [P, C.c_int],
     "fo_mesh_set_temperature": [P, P, C.c_double, C.c_double],
     "fo_set_lateral": [P, C.c_int],
+    "fo_spmv": [P, P, P, P, P, P],
+    "fo_line_factor": [P, P, P, P],
+    "fo_line_solve": [P, P, P, P],
+    "fo_krylov_dots": [P, I64, I32, P, I64, P, P, P],
+    "fo_krylov_update": [P, I64, I32, P, I64, P, P, P],
     "fo_last_launch_count": [P, P],
     "fo_kernel_timing": [P, I32],
     "fo_kernel_time_ms": [P, P, P],
