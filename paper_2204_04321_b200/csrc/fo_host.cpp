@@ -636,6 +636,7 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_plan.zero_cols);
   cudaFree(m->d_plan.blob);
   cudaFree(m->d_plan.blob_off);
+  cudaFree(m->d_plan.nedge);
   cudaFree(m->d_plan.multi);
   cudaFree(m->d_plan.partials);
   cudaFree(m->d_stage_U);

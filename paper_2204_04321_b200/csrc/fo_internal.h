@@ -81,6 +81,7 @@ struct PatchPlan {
   std::vector<uint32_t> contrib;     // encoded contribution (fo_plan.cpp contrib_code)
   std::vector<int32_t> zero_cols;    // boundary columns (zero-filled before the kernel)
   std::vector<MultiRec> multi;       // columns touched by >= 3 patches
+  std::vector<int32_t> nedge;        // [n_patches] leading edge pairs (two entries each)
   int32_t n_partials = 0;
 };
 
@@ -95,6 +96,7 @@ struct DevPatch {
   int32_t* zero_cols = nullptr;
   uint8_t* blob = nullptr;           // per-patch plan blobs (shared-memory layout)
   int64_t* blob_off = nullptr;       // [n_patches+1] byte offsets, multiples of 16
+  int32_t* nedge = nullptr;          // [n_patches]
   MultiRec* multi = nullptr;
   double* partials = nullptr;        // [n_partials][L+1][kPartialStride]
 };

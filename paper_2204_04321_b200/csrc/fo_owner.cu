@@ -33,6 +33,7 @@ struct PlanView {
   const int32_t* __restrict__ t_begin;
   const int32_t* __restrict__ col_ptr;
   const int32_t* __restrict__ pair_ptr;
+  const int32_t* __restrict__ nedge;
   const uint8_t* __restrict__ blob;      // per-patch plan blobs (fo_plan.cpp)
   const int64_t* __restrict__ blob_off;
   double* partials;   // multi columns' partial blocks (fo_plan.cpp)
@@ -82,6 +83,7 @@ struct SmemPlan {
   const PlanPair* pairs;
   const uint32_t* contrib;
   int ncols, npairs;
+  int nedge;   // pairs [0, nedge): edge slots, exactly two entries each
 };
 
 __device__ __forceinline__ void put2(double* dst, double x, double y, bool interior) {
@@ -108,78 +110,99 @@ __device__ __forceinline__ void put2(double* dst, double x, double y, bool inter
 // in L2).  Edge pairs (1-2 contributions) come first in the plan, self pairs
 // (one contribution per fan triangle) last, so loop lengths in a warp are
 // nearly uniform; consecutive slots of a column sit on consecutive lanes.
+// The 12 sums of one (column, slot) pair: level-kk rows x column level kk
+// (dg, from D), level-kk rows x level kk+1 (up, from O), level-kk+1 rows x
+// level kk (nx, from O transposed); [row comp a][column comp b].
+struct PairSums {
+  double dg[4], up[4], nx[4];
+};
+
+// add the two contributions c2 (one gather step) to s
 template <bool UP>
-__device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
-                                          const double* O, double* __restrict__ vals,
-                                          double* __restrict__ partials) {
+__device__ __forceinline__ void gather2(uint2 c2, const double* D, const double* O, PairSums& s) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t cb = h ? c2.y : c2.x;
+    const int tl = int(cb & 255);
+    const int pat = int((cb >> 13) & 3);
+    const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
+    const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
+    s.dg[0] += Dt[0];
+    s.dg[1] += Dt[sb];
+    s.dg[2] += Dt[sa];
+    s.dg[3] += Dt[sa + sb];
+    if (UP) {
+      const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
+      const double* On = O + int((cb >> 20) & 31) * TP + tl;
+      s.up[0] += Ou[0];
+      s.up[1] += Ou[TP];
+      s.up[2] += Ou[6 * TP];
+      s.up[3] += Ou[7 * TP];
+      s.nx[0] += On[0];
+      s.nx[1] += On[6 * TP];
+      s.nx[2] += On[TP];
+      s.nx[3] += On[7 * TP];
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_sums(PairSums& s) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s.dg[i] = s.up[i] = s.nx[i] = 0.0;
+}
+
+// write one pair's sums: plain stores (interior column) or RED (boundary),
+// or the patch's partial block (self slot of a multi column)
+template <bool UP>
+__device__ __forceinline__ void emit(const PlanPair& pp, const PlanCol& pc, const PairSums& s, int kk, int L,
+                                     double* __restrict__ vals, double* __restrict__ partials) {
   const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // column groups of level-kk rows
   const int m1 = (kk + 1 == L) ? 2 : 3;                   // column groups of level-kk+1 rows
   const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
   const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk-row slot
+  const int nc = pc.info & 255;
+  const bool interior = (pc.info >> 8) & 1;
+  if (((pc.info >> 30) & 1) && pp.slot == ((pc.info >> 9) & 255)) {
+    double2* q = reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride);
+    q[0] = make_double2(s.dg[0], s.dg[1]);
+    q[1] = make_double2(s.dg[2], s.dg[3]);
+    if (UP) {
+      q[2] = make_double2(s.up[0], s.up[1]);
+      q[3] = make_double2(s.up[2], s.up[3]);
+      q[4] = make_double2(s.nx[0], s.nx[1]);
+      q[5] = make_double2(s.nx[2], s.nx[3]);
+    }
+    return;
+  }
+  double* d0 = vals + pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
+  double* d1 = d0 + 2 * nc * m0;
+  put2(d0, s.dg[0], s.dg[1], interior);
+  put2(d1, s.dg[2], s.dg[3], interior);
+  if (UP) {
+    put2(d0 + 2, s.up[0], s.up[1], interior);
+    put2(d1 + 2, s.up[2], s.up[3], interior);
+    double* e0 = vals + pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
+    put2(e0, s.nx[0], s.nx[1], interior);
+    put2(e0 + 2 * nc * m1, s.nx[2], s.nx[3], interior);
+  }
+}
+
+template <bool UP>
+__device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
+                                          const double* O, double* __restrict__ vals,
+                                          double* __restrict__ partials) {
+  // edge pairs (exactly two entries) first, then self pairs (one entry per
+  // fan triangle, padded to even); a variant gathering two edge pairs per
+  // thread at a time measured slower (1.98 vs 1.91 ms)
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
-    const PlanCol& pc = sp.cols[pp.col];
-    double dg00 = 0.0, dg01 = 0.0, dg10 = 0.0, dg11 = 0.0;
-    double up00 = 0.0, up01 = 0.0, up10 = 0.0, up11 = 0.0;
-    double nx00 = 0.0, nx01 = 0.0, nx10 = 0.0, nx11 = 0.0;
+    PairSums s;
+    zero_sums(s);
     const uint32_t* cp = sp.contrib + pp.off;   // even count, 8-byte aligned
-#ifdef FO_EXPERIMENT_NO_GATHER
-    for (int e = 0; e < 0; e += 2) {
-#else
-    for (int e = 0; e < pp.cnt; e += 2) {
+#ifndef FO_EXPERIMENT_NO_GATHER
+    for (int e = 0; e < pp.cnt; e += 2) gather2<UP>(*reinterpret_cast<const uint2*>(cp + e), D, O, s);
 #endif
-      const uint2 c2 = *reinterpret_cast<const uint2*>(cp + e);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t cb = h ? c2.y : c2.x;
-        const int tl = int(cb & 255);
-        const int pat = int((cb >> 13) & 3);
-        const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
-        const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
-        dg00 += Dt[0];
-        dg01 += Dt[sb];
-        dg10 += Dt[sa];
-        dg11 += Dt[sa + sb];
-        if (UP) {
-          const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
-          const double* On = O + int((cb >> 20) & 31) * TP + tl;
-          up00 += Ou[0];
-          up01 += Ou[TP];
-          up10 += Ou[6 * TP];
-          up11 += Ou[7 * TP];
-          nx00 += On[0];
-          nx01 += On[6 * TP];
-          nx10 += On[TP];
-          nx11 += On[7 * TP];
-        }
-      }
-    }
-    const int nc = pc.info & 255;
-    const bool interior = (pc.info >> 8) & 1;
-    if (((pc.info >> 30) & 1) && pp.slot == ((pc.info >> 9) & 255)) {
-      // self slot of a multi column: this patch's partial block
-      double2* q = reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride);
-      q[0] = make_double2(dg00, dg01);
-      q[1] = make_double2(dg10, dg11);
-      if (UP) {
-        q[2] = make_double2(up00, up01);
-        q[3] = make_double2(up10, up11);
-        q[4] = make_double2(nx00, nx01);
-        q[5] = make_double2(nx10, nx11);
-      }
-      continue;
-    }
-    double* d0 = vals + pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
-    double* d1 = d0 + 2 * nc * m0;
-    put2(d0, dg00, dg01, interior);
-    put2(d1, dg10, dg11, interior);
-    if (UP) {
-      put2(d0 + 2, up00, up01, interior);
-      put2(d1 + 2, up10, up11, interior);
-      double* e0 = vals + pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
-      put2(e0, nx00, nx01, interior);
-      put2(e0 + 2 * nc * m1, nx10, nx11, interior);
-    }
+    emit<UP>(pp, sp.cols[pp.col], s, kk, L, vals, partials);
   }
 }
 
@@ -309,6 +332,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     sp.pairs = reinterpret_cast<const PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
     sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
     sp.ncols = c1 - c0; sp.npairs = q1 - q0;
+    sp.nedge = __ldg(pv.nedge + p);
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
   const int L = kp.L;
@@ -441,7 +465,7 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     if (st) return st;
     attr_set = true;
   }
-  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr,
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
               m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {

@@ -44,6 +44,7 @@ struct PatchBuild {
   std::vector<PlanCol> cols;
   std::vector<PlanPair> pairs;
   std::vector<uint32_t> contrib;
+  int32_t nedge = 0;   // pairs [0, nedge) are edge slots with exactly two entries
 };
 
 // Contribution of wedge-triangle tl (local vertex j = the row column, j2 = the
@@ -102,6 +103,8 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
       // even lengths: phase B gathers two contributions per step; the pad
       // entry reads triangle slot kPatchTris, kept zero by the kernel
       if (l.size() & 1) l.push_back(uint32_t(kPatchTris));
+      if (s != self && (interior || !l.empty()))   // edge slots: exactly two entries
+        while (l.size() < 2) l.push_back(uint32_t(kPatchTris));   // (interior slots of a part mesh may have none)
       if (s == self) {
         pc.self_off = uint16_t(B.contrib.size());
         pc.self_cnt = uint16_t(l.size());
@@ -121,6 +124,7 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
   // Edge slots have 1-2 contributions, self slots one per fan triangle (~6):
   // edge pairs first (column order, coalesced stores), then the self pairs, so
   // the lanes of a warp run loops of nearly equal length.
+  B.nedge = int32_t(B.pairs.size());
   B.pairs.insert(B.pairs.end(), self_pairs.begin(), self_pairs.end());
 }
 
@@ -171,6 +175,9 @@ fo_status build_patch_plan(fo_mesh m) {
       P.cols.insert(P.cols.end(), B.cols.begin(), B.cols.end());
       P.pairs.insert(P.pairs.end(), B.pairs.begin(), B.pairs.end());
       P.contrib.insert(P.contrib.end(), B.contrib.begin(), B.contrib.end());
+      for (int32_t q = 0; q < B.nedge; ++q)   // an edge joins <= 2 triangles: padded to 2
+        if (B.pairs[size_t(q)].cnt != 2) return FO_EINVAL;
+      P.nedge.push_back(B.nedge);
       P.col_ptr.push_back(int32_t(P.cols.size()));
       P.pair_ptr.push_back(int32_t(P.pairs.size()));
       P.contrib_ptr.push_back(int64_t(P.contrib.size()));
@@ -230,6 +237,7 @@ fo_status build_patch_plan(fo_mesh m) {
   if (!st) st = upload_vec(&m->d_plan.pair_ptr, P.pair_ptr);
   if (!st) st = upload_vec(&m->d_plan.blob, blob);
   if (!st) st = upload_vec(&m->d_plan.blob_off, blob_off);
+  if (!st) st = upload_vec(&m->d_plan.nedge, P.nedge);
   if (!st) st = upload_vec(&m->d_plan.zero_cols, P.zero_cols);
   if (!st) st = upload_vec(&m->d_plan.multi, P.multi);
   if (!st && P.n_partials > 0)
