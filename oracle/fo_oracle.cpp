@@ -85,6 +85,8 @@ struct Geo {           /* one wedge's data */
   double A;            /* flow factor of this wedge */
   bool basal;          /* k == 0 */
   int lateral;         /* bit jj: edge (jj, jj+1 mod 3) lies on the footprint boundary */
+  int tet;             /* NEXT-f4: 1 = three P1 tetrahedra instead of the wedge */
+  int ord[3];          /* local bottom nodes sorted by global vertex id (tet split) */
   int64_t gdof[12];    /* global DOFs, local dof = 2*i + a */
 };
 
@@ -134,6 +136,31 @@ double phys_grad(const double X[6][3], const double dN[6][3], double G[6][3]) {
   return det;
 }
 
+/* NEXT-f4: P1 tetrahedron `which` (0..2) of the wedge split by global vertex
+ * id (reading L22): with bottom nodes a < b < c (global ids) and tops a', b', c',
+ *   {a, b, c, c'}, {a, b, b', c'}, {a, a', b', c'};
+ * every quad side face (x < y) gets the diagonal x-bottom -- y-top, so
+ * neighbouring prisms split their shared face alike.  Returns, over the
+ * wedge's 6 local nodes, the centroid values N (1/4 on the tet's nodes, 0
+ * elsewhere), the constant physical gradients G (generic 3x3 inverse of the
+ * edge matrix) and the weight W = volume. */
+void tet_basis(const Geo& e, int which, double N[6], double G[6][3], double* W) {
+  const int a = e.ord[0], b = e.ord[1], c = e.ord[2];
+  const int nodes[3][4] = {{a, b, c, c + 3}, {a, b, b + 3, c + 3}, {a, a + 3, b + 3, c + 3}};
+  const int* nd = nodes[which];
+  double Xt[6][3] = {{0}};
+  double dN[6][3] = {{0}};
+  /* reference tet: N0 = 1 - xi - eta - zeta, N1 = xi, N2 = eta, N3 = zeta,
+   * evaluated through the 6-node interface (unused nodes: zero) */
+  const double dref[4][3] = {{-1, -1, -1}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int i = 0; i < 6; ++i) { N[i] = 0.0; for (int r = 0; r < 3; ++r) G[i][r] = 0.0; }
+  for (int q = 0; q < 4; ++q)
+    for (int r = 0; r < 3; ++r) { Xt[nd[q]][r] = e.X[nd[q]][r]; dN[nd[q]][r] = dref[q][r]; }
+  double det = phys_grad(Xt, dN, G);
+  for (int q = 0; q < 4; ++q) N[nd[q]] = 0.25;
+  *W = std::fabs(det) / 6.0;
+}
+
 /* Element residual r[12] (local dof 2i+a) and energy, templated on the scalar
  * type of U (double -> residual; Dual -> residual + Jacobian rows). */
 template <class T>
@@ -145,12 +172,21 @@ void element(const Geo& e, const ora_params& p, int terms, const T Ul[12], T r[1
   const double rg = p.rho * p.g;
   const double gz = 1.0 / std::sqrt(3.0);
   const double zq[2] = {-gz, gz};
-  for (int a = 0; a < 3; ++a) {
-    for (int sq = 0; sq < 2; ++sq) {
+  /* volume quadrature points: the wedge's 3 x 2 rule (reading L4), or for
+   * NEXT-f4 one centroid point per P1 tetrahedron (exact: constant gradients) */
+  const int n_pts = e.tet ? 3 : 6;
+  for (int pt = 0; pt < n_pts; ++pt) {
+    {
       double N[6], dN[6][3], G[6][3];
-      ref_basis(kTriXi[a], kTriEta[a], zq[sq], N, dN);
-      double det = phys_grad(e.X, dN, G);
-      double W = kTriW * 1.0 * det;               /* weights 1/6 (triangle) x 1 (Gauss) */
+      double W;
+      if (e.tet) {
+        tet_basis(e, pt, N, G, &W);
+      } else {
+        const int a = pt / 2, sq = pt % 2;
+        ref_basis(kTriXi[a], kTriEta[a], zq[sq], N, dN);
+        double det = phys_grad(e.X, dN, G);
+        W = kTriW * 1.0 * det;                    /* weights 1/6 (triangle) x 1 (Gauss) */
+      }
       /* velocity gradient */
       T ux = zero<T>(), uy = zero<T>(), uz = zero<T>(), vx = zero<T>(), vy = zero<T>(), vz = zero<T>();
       T u = zero<T>(), v = zero<T>();
@@ -280,6 +316,7 @@ int validate(const ora_mesh* m) {
   if (!m->xy || !m->tri || !m->thickness || !m->surface || !m->beta) return -1;
   if (m->p.glen_n <= 0.0 || m->p.A <= 0.0 || m->p.eps_reg < 0.0) return -1;
   if (m->T_star && !(m->A0 > 0.0)) return -1;
+  if (m->elem_type != 0 && m->elem_type != 1) return -1;
   const int L = m->n_layers;
   if (m->sigma) {
     if (m->sigma[0] != 0.0 || m->sigma[L] != 1.0) return -2;
@@ -346,6 +383,12 @@ void wedge_geo(const Mesh& M, int64_t t, int k, Geo& e) {
     e.A = m->A_elem ? m->A_elem[t * M.L + k] : m->p.A;
   e.basal = (k == 0);
   e.lateral = M.lateral.empty() ? 0 : M.lateral[t];
+  e.tet = m->elem_type == 1;
+  {   /* bottom local nodes by global vertex id (NEXT-f4 split) */
+    int o[3] = {0, 1, 2};
+    std::sort(o, o + 3, [&](int x, int y) { return v[x] < v[y]; });
+    for (int j = 0; j < 3; ++j) e.ord[j] = o[j];
+  }
 }
 
 /* footprint boundary edges: undirected edges used by exactly one triangle */

@@ -57,6 +57,9 @@ typedef struct {
   const double* T_star;     /* [n_tri*L] K, or NULL */
   double A0;                /* Pa^-n a^-1 */
   double Q_act;             /* J mol^-1 */
+  /* NEXT-f4: 0 = 6-node wedge (reading L5), 1 = three 4-node P1
+   * tetrahedra per prism, split by global vertex id (reading L22) */
+  int32_t elem_type;
 } ora_mesh;
 
 /* term mask for the pins: which integrals enter R / J / Pi */

@@ -41,7 +41,8 @@ class _Mesh(C.Structure):
                 ("tri", C.c_void_p), ("n_layers", C.c_int32), ("sigma", C.c_void_p),
                 ("thickness", C.c_void_p), ("surface", C.c_void_p), ("bed", C.c_void_p),
                 ("beta", C.c_void_p), ("A_elem", C.c_void_p), ("p", _Params),
-                ("T_star", C.c_void_p), ("A0", C.c_double), ("Q_act", C.c_double)]
+                ("T_star", C.c_void_p), ("A0", C.c_double), ("Q_act", C.c_double),
+                ("elem_type", C.c_int32)]
 
 
 _lib = None
@@ -104,7 +105,8 @@ class Oracle:
                         _ptr(self.beta), _ptr(self.A_elem),
                         _Params(prm["rho"], prm["g"], prm["rho_w"], prm["glen_n"],
                                 prm["eps_reg"], prm["A"], prm["H_min"]),
-                        _ptr(self.T_star), float(arr.get("A0", 0.0)), float(arr.get("Q", 0.0)))
+                        _ptr(self.T_star), float(arr.get("A0", 0.0)), float(arr.get("Q", 0.0)),
+                        int(getattr(fp, "elem_type", 0) or 0))
         self._graph = None
 
     @property

@@ -85,6 +85,7 @@ class Footprint:
     A_elem: np.ndarray | None = None
     T_star: np.ndarray | None = None    # NEXT-f3: per-wedge temperature (K)
     arrhenius: dict | None = None       # {"A0": Pa^-n a^-1, "Q": J/mol}
+    elem_type: int = 0                  # NEXT-f4: 0 wedge, 1 three P1 tetrahedra per prism
 
     @property
     def n_vert(self) -> int:
@@ -516,7 +517,7 @@ def sub_footprint(fp: Footprint, t0: int, t1: int) -> Footprint:
                      fp.beta[verts].copy(), Uv, dict(fp.params),
                      None if fp.A_elem is None else fp.A_elem.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy(),
                      None if fp.T_star is None else fp.T_star.reshape(fp.n_tri, -1)[t0:t1].reshape(-1).copy(),
-                     None if fp.arrhenius is None else dict(fp.arrhenius))
+                     None if fp.arrhenius is None else dict(fp.arrhenius), fp.elem_type)
 
 
 def sub_footprint_tris(fp: Footprint, tri_ids) -> Footprint:
@@ -535,7 +536,7 @@ def sub_footprint_tris(fp: Footprint, tri_ids) -> Footprint:
                     None if fp.bed is None else fp.bed[verts].copy(), fp.beta[verts].copy(), Uv,
                     dict(fp.params), A,
                     None if fp.T_star is None else fp.T_star.reshape(fp.n_tri, -1)[tri_ids].reshape(-1).copy(),
-                    None if fp.arrhenius is None else dict(fp.arrhenius))
+                    None if fp.arrhenius is None else dict(fp.arrhenius), fp.elem_type)
     sub.vertex_ids = verts
     return sub
 

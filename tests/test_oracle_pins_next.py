@@ -1,7 +1,8 @@
 """Pins of the oracle's NEXT rows against closed forms and
 invariants, like tests/test_oracle_pins.py:
   f1  lateral margin term (reading L12, quadrature L20),
-  f3  Arrhenius flow factor A = A0 exp(-Q / (R T*)).
+  f3  Arrhenius flow factor A = A0 exp(-Q / (R T*)),
+  f4  three P1 tetrahedra per prism (split rule: reading L22).
 PAPER.md line citations: P:n.
 """
 import numpy as np
@@ -158,3 +159,104 @@ def test_f3_temperature_is_per_wedge(ora_mod):
             dofs.update((2 * node, 2 * node + 1))
     changed = set(np.nonzero(R1 != R2)[0].tolist())
     assert changed and changed <= dofs
+
+
+# ---------------------------------------------------------------- f4
+# three P1 tetrahedra per prism, split by global vertex id (reading L22)
+def _tets(fp):
+    fp.elem_type = 1
+    return fp
+
+
+@pytest.mark.parametrize("n_glen", [1.0, 3.0])
+def test_f4_tet_patch_test(ora_mod, n_glen):
+    """Linear U, flat s, beta = 0 on distorted columns: interior residuals
+    vanish -- holds only if neighbouring prisms split their shared faces alike
+    (a non-conforming split breaks sum_e int grad phi_i = 0)."""
+    nx = 5
+    fp = _tets(mg.slab(nx=nx, n_layers=4, distort=0.25, params=dict(glen_n=n_glen)))
+    o = ora_mod.Oracle(fp)
+    L1 = fp.n_layers + 1
+    base = fp.surface - fp.thickness
+    z = (base[:, None] + fp.sigma[None, :] * fp.thickness[:, None]).reshape(-1)
+    x = np.repeat(fp.xy[:, 0], L1)
+    y = np.repeat(fp.xy[:, 1], L1)
+    U = np.zeros(o.n_dof)
+    U[0::2] = 3.0 + 2e-3 * x - 1e-3 * y + 0.05 * z
+    U[1::2] = -1.0 + 1e-3 * x + 4e-3 * y - 0.02 * z
+    R, M, _ = o.residual(U, terms=ora_mod.VISC)
+    col = np.arange(fp.n_vert)
+    edge = np.unique(np.concatenate([np.arange(nx + 1), np.arange(nx * (nx + 1), (nx + 1) ** 2),
+                                     np.arange(0, (nx + 1) ** 2, nx + 1), np.arange(nx, (nx + 1) ** 2, nx + 1)]))
+    k = np.arange(L1)
+    node_int = (~np.isin(col, edge)[:, None] & (k[None, :] > 0) & (k[None, :] < fp.n_layers)).reshape(-1)
+    dof_int = np.repeat(node_int, 2)
+    assert np.abs(R[dof_int]).max() <= 1e-12 * np.abs(M).max()
+    assert np.abs(R[~dof_int]).max() > 1e-6 * np.abs(M).max()
+
+
+def test_f4_tet_volume_and_driving_stress(ora_mod):
+    """The tets tile each prism exactly (vertical, hence planar, side faces):
+    sum_i R_{u,i}(U = 0) = rho g sum_t (ds/dx)_t |T_t| Hbar_t, as for wedges."""
+    fp = _tets(mg.ismip_hom_a(nx=6, n_layers=4))
+    fp.surface = fp.surface + 80.0 * np.sin(fp.xy[:, 1] / 9e3)
+    o = ora_mod.Oracle(fp)
+    R, _, _ = o.residual(np.zeros(o.n_dof), terms=ora_mod.BODY)
+    ex_u = 0.0
+    for t in fp.tri:
+        p = fp.xy[t]
+        twoA = (p[1, 0] - p[0, 0]) * (p[2, 1] - p[0, 1]) - (p[2, 0] - p[0, 0]) * (p[1, 1] - p[0, 1])
+        a = np.array([p[1, 1] - p[2, 1], p[2, 1] - p[0, 1], p[0, 1] - p[1, 1]]) / twoA
+        ex_u += 910.0 * 9.81 * np.dot(a, fp.surface[t]) * 0.5 * twoA * fp.thickness[t].mean()
+    assert abs(R[0::2].sum() - ex_u) <= 1e-12 * abs(ex_u)
+
+
+def test_f4_tet_nullspace_symmetry_fd(ora_mod):
+    """beta = 0 rigid nullspace, J = J^T, FD Jacobian and FD energy for tets."""
+    fp = _tets(mg.greenland_like(100.0, n_layers=3))
+    o = ora_mod.Oracle(fp)
+    J = o.dense_jacobian(fp.U, terms=ora_mod.VISC)
+    L1 = fp.n_layers + 1
+    x = np.repeat(fp.xy[:, 0], L1)
+    y = np.repeat(fp.xy[:, 1], L1)
+    for w in (np.tile([1.0, 0.0], o.n_dof // 2), np.tile([0.0, 1.0], o.n_dof // 2),
+              np.stack([-y, x], axis=1).reshape(-1)):
+        assert np.abs(J @ w).max() <= 1e-12 * np.abs(J).max() * np.abs(w).max()
+    Jf = o.dense_jacobian(fp.U)
+    assert np.abs(Jf - Jf.T).max() <= 1e-14 * np.abs(Jf).max()
+    U = fp.U
+    R = o.residual(U)[0]
+    for j in np.linspace(0, o.n_dof - 1, 12).astype(int):
+        h = 1e-6 * max(1.0, abs(U[j]))
+        Up, Um = U.copy(), U.copy()
+        Up[j] += h
+        Um[j] -= h
+        fd = (o.residual(Up)[0] - o.residual(Um)[0]) / (2 * h)
+        assert np.abs(Jf[:, j] - fd).max() <= 1e-6 * np.abs(Jf[:, j]).max()
+        he = 1e-4 * max(1.0, abs(U[j]))
+        Up, Um = U.copy(), U.copy()
+        Up[j] += he
+        Um[j] -= he
+        fde = (o.energy(Up, dof=j) - o.energy(Um, dof=j)) / (2 * he)
+        assert abs(fde - R[j]) <= 1e-6 * np.abs(R).max()
+
+
+def test_f4_tet_structural_zeros(ora_mod):
+    """Inside each prism the split couples 12 of the 15 node pairs: the pairs
+    (a', b), (a', c), (b', c) (a < b < c by global id) get exact zeros in J."""
+    fp = _tets(mg.ismip_hom_a(nx=3, n_layers=2))
+    o = ora_mod.Oracle(fp)
+    J = o.dense_jacobian(fp.U)
+    L1 = fp.n_layers + 1
+    zero_pairs = nonzero_pairs = 0
+    for t in fp.tri:
+        a, b, c = sorted(int(v) for v in t)
+        for k in range(fp.n_layers):
+            nd = lambda v, lev: v * L1 + k + lev
+            for (p, q) in [(nd(a, 1), nd(b, 0)), (nd(a, 1), nd(c, 0)), (nd(b, 1), nd(c, 0))]:
+                blk = J[2 * p:2 * p + 2, 2 * q:2 * q + 2]
+                # another prism may couple them (as bottom/top of its own split)
+                zero_pairs += int(np.all(blk == 0.0))
+            blk = J[2 * nd(a, 1):2 * nd(a, 1) + 2, 2 * nd(c, 1):2 * nd(c, 1) + 2]
+            nonzero_pairs += int(np.any(blk != 0.0))
+    assert zero_pairs > 0 and nonzero_pairs == len(fp.tri) * fp.n_layers
