@@ -163,6 +163,17 @@ FO_API fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, 
 FO_API fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, double* h_R,
                                     double* h_vals, void* stream);
 
+/* NEXT-f4: element of the prism layers.  FO_ELEM_WEDGE (default) is
+ * the 6-node wedge (reading L5); FO_ELEM_TET3 splits every prism into three
+ * P1 tetrahedra by GLOBAL vertex id (reading L22: with corners a < b < c,
+ * {a,b,c,c'}, {a,b,b',c'}, {a,a',b',c'}), one quadrature point each, exact
+ * Jacobian; it assembles into the same graph (3 of the 15 node pairs of a
+ * prism become structural zeros) with the owner-computes scatter only.
+ * FO_EINVAL for an unknown type, for TET3 with the lateral term enabled
+ * (fo_set_lateral) or with FO_SCATTER_ATOMIC. */
+typedef enum { FO_ELEM_WEDGE = 0, FO_ELEM_TET3 = 1 } fo_element;
+FO_API fo_status fo_set_element(fo_mesh m, fo_element type);
+
 /* ---- NEXT-f2: the Newton consumer of the assembled Jacobian ----
  * Single-domain meshes only (FO_ESTATE for a part mesh).  All buffers are
  * caller-owned contiguous fp64 device arrays of n_dofs entries unless stated;

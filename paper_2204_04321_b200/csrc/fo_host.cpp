@@ -205,6 +205,12 @@ fo_status build_topology(int64_t n_vert, int64_t n_tri, const int32_t* tri, int3
   for (int64_t t = 0; t < nt; ++t) {
     TriRec& r = T.trirec[size_t(t)];
     for (int i = 0; i < 3; ++i) r.v[i] = T.tri[3 * t + i];
+    {   // NEXT-f4 split order: local corners by GLOBAL vertex id (reading L22)
+      const int32_t* g = tri + 3 * T.tri_glob[size_t(t)];
+      int o[3] = {0, 1, 2};
+      std::sort(o, o + 3, [&](int x, int y) { return g[x] < g[y]; });
+      r.pad[0] = uint8_t(o[0] | (o[1] << 2) | (o[2] << 4));
+    }
     for (int i = 0; i < 3; ++i) {
       const int32_t ci = r.v[i];
       const int32_t* b = T.nbr.data() + T.nbr_ptr[size_t(ci)];
@@ -568,12 +574,25 @@ fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, do
 
 fo_status fo_set_lateral(fo_mesh m, int enable) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (enable && m->elem_type != FO_ELEM_WEDGE)
+    return fail(FO_EINVAL, "the lateral term is defined on wedge faces (FO_ELEM_WEDGE only)");
   m->lateral = enable != 0;
+  return FO_OK;
+}
+
+fo_status fo_set_element(fo_mesh m, fo_element type) {
+  if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (type != FO_ELEM_WEDGE && type != FO_ELEM_TET3) return fail(FO_EINVAL, "unknown element type");
+  if (type == FO_ELEM_TET3 && (m->lateral || m->scatter != FO_SCATTER_OWNER))
+    return fail(FO_EINVAL, "FO_ELEM_TET3 needs the owner scatter and no lateral term");
+  m->elem_type = type;
   return FO_OK;
 }
 
 fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (s != FO_SCATTER_OWNER && m->elem_type != FO_ELEM_WEDGE)
+    return fail(FO_EINVAL, "the atomic scatter supports FO_ELEM_WEDGE only");
   if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC) return fail(FO_EINVAL, "bad scatter");
   m->scatter = s;
   return FO_OK;

@@ -25,7 +25,7 @@ struct alignas(16) ColRec {
 struct alignas(8) TriRec {
   int32_t v[3];
   uint8_t slot[9];
-  uint8_t pad[3];
+  uint8_t pad[3];   // pad[0]: corners sorted by global vertex id, 2 bits each (NEXT-f4)
 };
 
 // Triangles per patch of the owner-computes kernel (one thread per triangle
@@ -134,6 +134,7 @@ struct fo_mesh_s {
   double* d_A = nullptr;           // per-wedge A^(-1/n) or nullptr
   double* d_T = nullptr;           // per-wedge T* (NEXT-f3) or nullptr
   double A0fac = 0.0, QnR = 0.0;   // Arrhenius constants folded for the kernels
+  int elem_type = FO_ELEM_WEDGE;   // NEXT-f4 (fo_element_tet.cuh)
   // NEXT-f1 lateral margin term (fo_lateral.cu)
   bool lateral = false;
   int32_t n_lat_cols = 0, n_lat_faces = 0;

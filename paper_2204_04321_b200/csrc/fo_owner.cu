@@ -22,6 +22,7 @@
 
 #include "fo_element.cuh"
 #include "fo_element_v4.cuh"
+#include "fo_element_tet.cuh"
 
 #include <type_traits>
 #include "fo_internal.h"
@@ -307,7 +308,7 @@ struct SmemCmp {
   __device__ __forceinline__ double& operator()(int i) { return base[i * TP + tl]; }
 };
 
-template <bool NEED_J, bool N3>
+template <bool NEED_J, bool N3, bool TET>
 __global__ void __launch_bounds__(kPatchTris, kPatchCtasPerSm)
 ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
                 const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
@@ -344,6 +345,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     const int* tp = reinterpret_cast<const int*>(tris + (t0 + tl));
     const int2 v01 = __ldg(reinterpret_cast<const int2*>(tp));
     tr.v[0] = v01.x; tr.v[1] = v01.y; tr.v[2] = __ldg(tp + 2);
+    if (TET) tr.pad[0] = uint8_t((__ldg(tp + 5) >> 8) & 0xff);   // NEXT-f4 split order
 #pragma unroll
     for (int i = 0; i < kD; ++i) D[i * TP + tl] = 0.0;
   }
@@ -366,7 +368,8 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       WedgeIn w;
       wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
       SmemCmp cmp{C, tl};
-      wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
+      if constexpr (TET) tet3_element<N3>(w, tr.pad[0], kp.rg, kp.eps, kp.glen_n, sk);
+      else wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
     }
     if (k == 0) bulk_wait(&plan_bar);
     __syncthreads();
@@ -454,12 +457,12 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
 
 static size_t smem_bytes(bool) { return size_t(kPlanOffset) + kPlanBytes; }
 
-template <bool NEED_J, bool N3>
+template <bool NEED_J, bool N3, bool TET>
 static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
   static bool attr_set = false;
   const size_t sm = smem_bytes(NEED_J);
   if (!attr_set) {
-    fo_status st = cuda_status(cudaFuncSetAttribute(ka_patch_kernel<NEED_J, N3>,
+    fo_status st = cuda_status(cudaFuncSetAttribute(ka_patch_kernel<NEED_J, N3, TET>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
                                "cudaFuncSetAttribute");
     if (st) return st;
@@ -473,7 +476,7 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  ka_patch_kernel<NEED_J, N3><<<m->plan.n_patches, kPatchTris, sm, s>>>(
+  ka_patch_kernel<NEED_J, N3, TET><<<m->plan.n_patches, kPatchTris, sm, s>>>(
       m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R, vals);
   if (m->timing) {
     cudaEventRecord(e1, s);
@@ -512,9 +515,13 @@ fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals
   const bool n3 = m->p.glen_n == 3.0;
   fo_status st;
   if (need_j)
-    st = n3 ? launch_patch<true, true>(m, d_U, R, d_vals, s) : launch_patch<true, false>(m, d_U, R, d_vals, s);
+    st = m->elem_type == FO_ELEM_TET3
+             ? (n3 ? launch_patch<true, true, true>(m, d_U, R, d_vals, s) : launch_patch<true, false, true>(m, d_U, R, d_vals, s))
+             : (n3 ? launch_patch<true, true, false>(m, d_U, R, d_vals, s) : launch_patch<true, false, false>(m, d_U, R, d_vals, s));
   else
-    st = n3 ? launch_patch<false, true>(m, d_U, R, nullptr, s) : launch_patch<false, false>(m, d_U, R, nullptr, s);
+    st = m->elem_type == FO_ELEM_TET3
+             ? (n3 ? launch_patch<false, true, true>(m, d_U, R, nullptr, s) : launch_patch<false, false, true>(m, d_U, R, nullptr, s))
+             : (n3 ? launch_patch<false, true, false>(m, d_U, R, nullptr, s) : launch_patch<false, false, false>(m, d_U, R, nullptr, s));
   if (st) return st;
   ++launches;
   const int nm = int(m->plan.multi.size());

@@ -61,6 +61,7 @@ _SIGS = {
     "fo_set_scatter": [P, C.c_int],
     "fo_mesh_set_temperature": [P, P, C.c_double, C.c_double],
     "fo_set_lateral": [P, C.c_int],
+    "fo_set_element": [P, C.c_int],
     "fo_spmv": [P, P, P, P, P, P],
     "fo_line_factor": [P, P, P, P],
     "fo_line_solve": [P, P, P, P],
@@ -342,6 +343,10 @@ class Mesh:
         T = np.ascontiguousarray(T_star, dtype=np.float64)
         check(lib().fo_mesh_set_temperature(self.handle, T.ctypes.data, float(A0), float(Q)),
               "fo_mesh_set_temperature")
+
+    def set_element(self, elem_type: int):
+        """NEXT-f4: 0 = wedge (default), 1 = three P1 tetrahedra per prism."""
+        check(lib().fo_set_element(self.handle, int(elem_type)), "fo_set_element")
 
     def set_lateral(self, on: bool = True):
         """NEXT-f1: include the lateral margin term in R."""

@@ -27,6 +27,8 @@ def torch_cuda():
 def gpu_assemble(torch, fp, params=None, scatter=None, lateral=False):
     from paper_2204_04321_b200 import fo
     mesh = fo.Mesh.from_footprint(fp, params=params)
+    if getattr(fp, "elem_type", 0):
+        mesh.set_element(fp.elem_type)
     if lateral:
         mesh.set_lateral(True)
     if scatter is not None:
@@ -145,6 +147,61 @@ def test_parity_lateral_margin_term(torch_cuda, ora_mod, case, scatter):
     Rb, Mb, _ = o.residual(np.zeros(fp.n_dof), terms=ora_mod.BODY | ora_mod.LATERAL)
     assert np.abs(Rl).max() > 0.0
     assert np.abs((R_on - R_off) - Rl).max() <= R_TOL * np.abs(Mb).max()
+
+
+@pytest.mark.parametrize("case", ["C1", "gris-40km", "slab-distorted", "C5-small", "C2"])
+def test_parity_tetrahedra(torch_cuda, ora_mod, case):
+    """NEXT-f4: three P1 tetrahedra per prism (reading L22)."""
+    fp = {"C1": mg.ismip_hom_a,
+          "gris-40km": lambda: mg.greenland_like(40.0),
+          "slab-distorted": lambda: mg.slab(nx=7, n_layers=4, distort=0.25),
+          "C5-small": lambda: mg.antarctica_like(D_km=150.0, n_layers=3),
+          "C2": lambda: mg.greenland_like(16.0)}[case]()
+    if case == "C5-small":
+        fp = mg.sub_footprint(fp, 0, min(fp.n_tri, 6000))
+    fp.elem_type = 1
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+def test_tetrahedra_partitioned_and_rejections(torch_cuda, ora_mod):
+    """f4 on a 2-part partition (owned rows after the halo plan's sums equal
+    the single-domain tet assembly); unsupported combinations are rejected."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like(40.0, n_layers=4)
+    fp.elem_type = 1
+    L, P = fp.n_layers, 2
+    full = fo.Mesh.from_footprint(fp)
+    full.set_element(1)
+    Rf, Vf = full.jacobian(torch.tensor(fp.U, device="cuda"))
+    Rf = Rf.cpu().numpy()
+    part = fo.partition(fp.n_tri, P)
+    outs, meshes = [], []
+    for p in range(P):
+        m = fo.Mesh.from_footprint(fp, part=part, my_part=p, n_parts=P)
+        m.set_element(1)
+        glob, nA, nB, nC = m.columns()
+        Ul = fp.U.reshape(fp.n_vert, L + 1, 2)[glob].reshape(-1)
+        outs.append(list(m.jacobian(torch.tensor(Ul, device="cuda"))))
+        meshes.append((m, glob))
+    plans = [fo.halo_plan_host(fp.n_vert, fp.tri, L, part, P, p) for p in range(P)]
+    for p in range(P):
+        for q, (sr, dr, sv, dv) in plans[p].items():
+            outs[q][0].index_add_(0, torch.tensor(dr, device="cuda"), outs[p][0][torch.tensor(sr, device="cuda")])
+    torch.cuda.synchronize()
+    for p in range(P):
+        m, glob = meshes[p]
+        L1 = L + 1
+        gd = np.stack([2 * (glob[:, None] * L1 + np.arange(L1)), 2 * (glob[:, None] * L1 + np.arange(L1)) + 1],
+                      axis=2).reshape(-1)
+        R = outs[p][0].cpu().numpy()
+        n = m.n_owned_dofs
+        assert np.abs(R[:n] - Rf[gd[:n]]).max() <= 1e-12 * np.abs(Rf).max()
+    with pytest.raises(fo.FoError):
+        full.set_lateral(True)
+    with pytest.raises(fo.FoError):
+        full.set_scatter(1)
 
 
 @pytest.mark.parametrize("L", [1, 2, 17])
