@@ -45,8 +45,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scatter", type=int, default=0, help="0 owner-computes (default), 1 atomic")
-    ap.add_argument("--cpu-sample-tris", type=int, default=40000)
-    ap.add_argument("--ref-sample-tris", type=int, default=3000)
+    ap.add_argument("--cpu-sample-tris", type=int, default=40000, help="oracle sample per host core")
+    ap.add_argument("--ref-sample-tris", type=int, default=3000, help="reference-arm sample per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     return ap.parse_args()
@@ -137,54 +137,92 @@ def ncu_summary(config_name):
     return d if d.get("config") == config_name else None
 
 
-def cpu_baseline_oracle(fp, n_tri_sample):
-    """The oracle (serial C++, Dual<12> AD Jacobian) on the first n_tri_sample
-    Hilbert-contiguous triangles of the same workload, on 1 host core."""
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+_FORK_FP = None   # the workload, inherited by the forked oracle processes
+
+
+def _oracle_worker(args):
+    """one process: the oracle's R + Dual<12> Jacobian on one Hilbert-contiguous
+    part of the sample (graph built untimed), `reps` timed calls after a common
+    start barrier; returns the seconds of each call."""
+    t0, t1, reps, barrier = args
+    fp = _FORK_FP
     from oracle import oracle as ora
     from paper_2204_04321_b200 import meshgen as mg
-    ora.build()
-    sub = mg.sub_footprint(fp, 0, min(n_tri_sample, fp.n_tri))
+    sub = mg.sub_footprint(fp, t0, t1)
     o = ora.Oracle(sub)
-    o.graph()                                  # brute-force graph: setup, untimed
-    t0 = time.perf_counter()
-    o.jacobian(sub.U)
-    dt = time.perf_counter() - t0
-    return {"value": sub.n_elem / dt / 1e6, "unit": "Melem/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {sub.n_tri} triangles x {sub.n_layers} layers = {sub.n_elem} wedges of "
-                      f"{fp.name}: oracle residual + Dual<12> AD Jacobian (one call, {dt:.2f} s, serial, -O2)",
+    o.graph()
+    barrier.wait()
+    out = []
+    for _ in range(reps):
+        a = time.perf_counter()
+        o.jacobian(sub.U)
+        out.append(time.perf_counter() - a)
+    return out
+
+
+def oracle_parallel(fp, n_tri_sample, procs, reps=1):
+    """SURVEY.md 8(d) d5 (all cores): P processes, one per host core, each
+    assembling one Hilbert-contiguous part of the sample (the paper's MPI
+    rank per core); per call the slowest process's time counts.
+    Returns (seconds per call for each rep, sample triangles, wedges)."""
+    import multiprocessing as mp
+    from oracle import oracle as ora
+    global _FORK_FP
+    ora.build()
+    _FORK_FP = fp
+    nt = min(n_tri_sample, fp.n_tri)
+    procs = max(1, min(procs, nt))
+    ctx = mp.get_context("fork")
+    barrier = ctx.Manager().Barrier(procs)
+    bounds = [(i * nt) // procs for i in range(procs + 1)]
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_oracle_worker, [(bounds[i], bounds[i + 1], reps, barrier) for i in range(procs)], chunksize=1)
+    per_rep = [max(r[k] for r in res) for k in range(reps)]
+    return per_rep, nt, nt * fp.n_layers
+
+
+def cpu_baseline_oracle(fp, n_tri_sample_per_core):
+    """The oracle as it stands (serial C++ per process, Dual<12> AD Jacobian) on
+    every host core: a sample of n_tri_sample_per_core triangles per core (the
+    whole workload if smaller), split into Hilbert-contiguous parts."""
+    cores = _host_cores()
+    secs, nt, nw = oracle_parallel(fp, n_tri_sample_per_core * cores, cores)
+    dt = secs[0]
+    return {"value": nw / dt / 1e6, "unit": "Melem/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {nt} triangles x {fp.n_layers} layers = {nw} wedges of {fp.name}, split into "
+                      f"{cores} Hilbert-contiguous parts, one oracle process per core (R + Dual<12> AD "
+                      f"Jacobian, -O2); wall time of the slowest process {dt:.2f} s",
             "seconds": dt}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only),
+    one process per core on a Hilbert-contiguous split of a bounded sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     fp, name = workload(args.gpus)
-    from oracle import oracle as ora
-    from paper_2204_04321_b200 import meshgen as mg
-    ora.build()
-    sub = mg.sub_footprint(fp, 0, min(args.ref_sample_tris, fp.n_tri))
-    o = ora.Oracle(sub)
-    o.graph()
-    for _ in range(args.warmup):
-        o.jacobian(sub.U)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        o.jacobian(sub.U)
-        times.append(time.perf_counter() - t0)
+    cores = _host_cores()
+    secs, nt, nw = oracle_parallel(fp, args.ref_sample_tris * cores, cores, reps=args.warmup + args.steps)
+    times = secs[args.warmup:]
     tot = sum(times)
-    value = sub.n_elem * args.steps / tot / 1e6
-    sample = (f"{sub.n_elem} wedges per step (first {sub.n_tri} triangles of {fp.name}), "
-              f"serial oracle R + Dual<12> AD Jacobian")
+    value = nw * args.steps / tot / 1e6
+    sample = (f"{nw} wedges per step (first {nt} triangles of {fp.name}) split over {cores} host cores, "
+              f"one oracle process per core, R + Dual<12> AD Jacobian")
     line = {"metric": METRIC, "value": value, "unit": "Melem/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{name}: {fp.name}, sample of {sub.n_tri} triangles x {sub.n_layers} layers",
-                       "n_elem": sub.n_elem},
-            "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {"workload": f"{name}: {fp.name}, sample of {nt} triangles x {fp.n_layers} layers",
+                       "n_elem": nw},
+            "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
