@@ -382,3 +382,37 @@ def test_c3_bitwise_reproducible_and_overwritten(torch_cuda):
         assert not torch.isnan(R).any() and not torch.isnan(vals).any() and not torch.isnan(Rr).any()
         outs.append((R.cpu().numpy().tobytes(), vals.cpu().numpy().tobytes(), Rr.cpu().numpy().tobytes()))
     assert outs[0] == outs[1] == outs[2]
+
+
+def test_assembly_captures_into_a_cuda_graph(torch_cuda):
+    """No host synchronisation inside fo_assemble_jacobian: the whole call
+    (zero-fill, patch kernel, fix-up) captures into a CUDA graph whose replay
+    equals the eager assembly bit for bit, also after U changes in place."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like(30.0, n_layers=6)
+    mesh = fo.Mesh.from_footprint(fp)
+    g = mesh.graph()
+    U = torch.tensor(fp.U, device="cuda")
+    R, V = mesh.jacobian(U)                       # eager (also first-call setup)
+    Rg = torch.empty_like(R)
+    Vg = torch.empty_like(V)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        mesh.jacobian(U, R=Rg, vals=Vg)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        mesh.jacobian(U, R=Rg, vals=Vg)
+    Rg.fill_(float("nan"))
+    Vg.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Rg, R) and torch.equal(Vg, V)
+    U.mul_(1.5)
+    R2, V2 = mesh.jacobian(U)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Rg, R2) and torch.equal(Vg, V2)
+    assert not torch.equal(R2, R)
