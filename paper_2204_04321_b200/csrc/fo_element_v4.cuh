@@ -151,6 +151,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   {
     const double ex1 = (1.0 - glen_n) / (2.0 * glen_n);
     const double kap = (glen_n - 1.0) / (2.0 * glen_n);
+    double qe[6];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
@@ -165,26 +166,31 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         const double exy = 0.5 * (uy + vx), exz = 0.5 * uz[a], eyz = 0.5 * vz[a];
         // effective strain rate squared, eq:effeps
         const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
-        const double qe = qq + eps;
-        const double W = W0 * zz[a];
-        double c, d;
-        if (N3) {
-          const double y = rcbrt(qe);                  // (q + eps)^(-1/3)
-          c = W * w.Afac * y;                           // w_q 2 mu_q
-          d = c * (y * y * y) * (1.0 / 3.0);            // c (n-1)/(2n) / (q+eps)
-        } else {
-          c = W * w.Afac * pow(qe, ex1);
-          d = c * kap / qe;
-        }
+        qe[q] = qq + eps;
         // strain-rate vectors
         const double e1x = 2.0 * ux + vy, e1y = exy, e1z = exz;
         const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
         Qu(q) = e1z - e1x * zx - e1y * zy;
         Qv(q) = e2z - e2x * zx - e2y * zy;
         E1x(q) = e1x; E1y(q) = e1y; E2y(q) = e2y;   // e2x == e1y
-        cq[q] = c;
-        dq(q) = d;
       }
+    }
+    // the six viscosities together: independent rcbrt chains interleave
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int a = q >> 1;
+      const double W = W0 * (a == 0 ? zz[0] : (a == 1 ? zz[1] : zz[2]));
+      double c, d;
+      if (N3) {
+        const double y = rcbrt(qe[q]);               // (q + eps)^(-1/3)
+        c = W * w.Afac * y;                           // w_q 2 mu_q
+        d = c * (y * y * y) * (1.0 / 3.0);            // c (n-1)/(2n) / (q+eps)
+      } else {
+        c = W * w.Afac * pow(qe[q], ex1);
+        d = c * kap / qe[q];
+      }
+      cq[q] = c;
+      dq(q) = d;
     }
   }
   // ---- frozen-viscosity part in closed form from the six c_q
