@@ -218,6 +218,25 @@ def test_single_triangle(torch_cuda, ora_mod):
     check_parity(ora_mod.Oracle(fp), g, fp=fp)
 
 
+@pytest.mark.parametrize("spokes", [80, 200])
+def test_high_degree_vertex(torch_cuda, ora_mod, spokes):
+    """A wheel: one column coupled to `spokes` neighbours (row nnz 6 (spokes+1),
+    one or two patches around it), the maximum-degree case of the plan."""
+    rng = mg.SplitMix64(21)
+    th = 2 * np.pi * np.arange(spokes) / spokes
+    xy = np.vstack([[0.0, 0.0], np.stack([2e4 * np.cos(th), 2e4 * np.sin(th)], axis=1)])
+    tri = np.array([[0, 1 + i, 1 + (i + 1) % spokes] for i in range(spokes)], dtype=np.int32)
+    nv, L = xy.shape[0], 4
+    H = 900.0 + 200.0 * rng.uniform(nv)
+    s_ = 1200.0 + 1e-2 * xy[:, 0]
+    beta = 100.0 + 900.0 * rng.uniform(nv)
+    U = 20.0 * rng.normal(2 * nv * (L + 1)) + 40.0
+    fp = mg.Footprint("wheel", xy, tri, np.linspace(0.0, 1.0, L + 1), H, s_, None, beta, U,
+                      dict(mg.DEFAULT_PARAMS))
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
 def test_empty_mesh(torch_cuda):
     from paper_2204_04321_b200 import fo
     fp = mg.ismip_hom_a(nx=2, n_layers=2)
@@ -269,12 +288,14 @@ def test_host_buffer_entry_point(torch_cuda):
     assert np.abs(Vh.numpy() - Vd.cpu().numpy()).max() <= 1e-13 * np.abs(Vh.numpy()).max()
 
 
-def test_c3_full_size_sampled(torch_cuda, ora_mod):
-    """C3 at its full size in the bench's launch configuration: complete rows of
-    sampled columns vs the oracle on the sub-footprint of their triangle fans."""
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
+    """C3 (and C5, with its floating shelves) at full size in the bench's launch
+    configuration: complete rows of sampled columns vs the oracle on the
+    sub-footprint of their triangle fans."""
     import torch
     from paper_2204_04321_b200 import fo
-    fp = mg.greenland_like_1_10()
+    fp = mg.greenland_like_1_10() if cfg == "C3" else mg.antarctica_like()
     mesh = fo.Mesh.from_footprint(fp)
     U = torch.tensor(fp.U, device="cuda")
     g = mesh.graph()
