@@ -45,5 +45,22 @@ d = {"config": cfg, "kernel": h and v[h.index("Kernel Name")] if "Kernel Name" i
      "fp64_instr_per_wedge": {k: c / nw for k, c in cnt.items()},
      "fp64_flop_per_wedge": flops / nw}
 d["dram_bytes_per_launch"] = d["dram_bytes_read"] + d["dram_bytes_write"]
+
+
+def raw(name):
+    return float(v[h.index(name)].replace(",", "")) if name in h else None
+
+
+# SURVEY.md 8(d) d4 report items
+d["fp64_pipe_pct"] = raw("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed")
+d["registers_per_thread"] = raw("launch__registers_per_thread")
+d["warps_active_pct"] = raw("sm__warps_active.avg.pct_of_peak_sustained_active")
+d["l1_data_pipe_pct"] = raw("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed")
+d["shared_wavefronts"] = raw("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+d["shared_bank_conflicts"] = raw("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")
+red = raw("lts__t_sectors_srcunit_tex_op_red.sum")
+d["l2_red_sectors"] = red
+if red is not None:
+    d["l2_red_sectors_per_s"] = red / (d["gpu_time_ms"] / 1e3)
 json.dump(d, open(out, "w"), indent=1)
 print(json.dumps(d, indent=1))
