@@ -36,7 +36,9 @@ __device__ __forceinline__ void r_top_add_rt(Sink& sink, int p, double v) {
     if (q == p) sink.r_top_add(q, v);
 }
 
-template <bool N3, class Sink>
+// SORTED: the corners already are in global-id order (fo_set_element permutes
+// the triangle records), so every node index below is a compile-time constant
+template <bool N3, bool SORTED, class Sink>
 __device__ __forceinline__ void tet3_element(const WedgeIn& w, int order, double rg, double eps, double glen_n,
                                              Sink& sink) {
   // fresh top block, bottom-top block and top residual (the sink adds below)
@@ -50,9 +52,9 @@ __device__ __forceinline__ void tet3_element(const WedgeIn& w, int order, double
   }
   // node positions relative to corner 0 (vertical columns: x, y per corner)
   const double X[3] = {0.0, w.e1x, w.e2x}, Y[3] = {0.0, w.e1y, w.e2y};
-  const int ca = order & 3, cb = (order >> 2) & 3, cc = (order >> 4) & 3;
+  const int ca = SORTED ? 0 : order & 3, cb = SORTED ? 1 : (order >> 2) & 3, cc = SORTED ? 2 : (order >> 4) & 3;
   const double ex1 = (1.0 - glen_n) / (2.0 * glen_n), kap = (glen_n - 1.0) / (2.0 * glen_n);
-#pragma unroll 1
+#pragma unroll
   for (int t = 0; t < 3; ++t) {
     // wedge-local nodes (corner + 3 * level) of tet t
     int nd[4];

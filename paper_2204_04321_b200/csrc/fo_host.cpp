@@ -585,8 +585,40 @@ fo_status fo_set_element(fo_mesh m, fo_element type) {
   if (type != FO_ELEM_WEDGE && type != FO_ELEM_TET3) return fail(FO_EINVAL, "unknown element type");
   if (type == FO_ELEM_TET3 && (m->lateral || m->scatter != FO_SCATTER_OWNER))
     return fail(FO_EINVAL, "FO_ELEM_TET3 needs the owner scatter and no lateral term");
-  m->elem_type = type;
-  return FO_OK;
+  if (type == m->elem_type) return FO_OK;
+  // The tetrahedral element runs with every triangle's corners in global-id
+  // order (its split rule, reading L22, then has compile-time nodes); the
+  // wedge needs the caller's CCW order back.  Either way the patch plan is
+  // rebuilt for the new corner order.
+  fo_status st = cuda_status(cudaSetDevice(m->device), "cudaSetDevice");
+  if (st) return st;
+  if (type == FO_ELEM_TET3) {
+    m->tri_ccw = m->tri;
+    m->trirec_ccw = m->trirec;
+    for (int64_t t = 0; t < m->n_tri; ++t) {
+      const TriRec o = m->trirec_ccw[size_t(t)];
+      const int ord[3] = {o.pad[0] & 3, (o.pad[0] >> 2) & 3, (o.pad[0] >> 4) & 3};
+      TriRec& r = m->trirec[size_t(t)];
+      for (int k = 0; k < 3; ++k) {
+        r.v[k] = o.v[ord[k]];
+        m->tri[size_t(3 * t + k)] = m->tri_ccw[size_t(3 * t + ord[k])];
+        for (int l = 0; l < 3; ++l) r.slot[3 * k + l] = o.slot[3 * ord[k] + ord[l]];
+      }
+      r.pad[0] = uint8_t(0 | (1 << 2) | (2 << 4));
+    }
+  } else {
+    m->tri.swap(m->tri_ccw);
+    m->trirec.swap(m->trirec_ccw);
+    m->tri_ccw.clear();
+    m->trirec_ccw.clear();
+  }
+  if (!m->trirec.empty())
+    st = cuda_status(cudaMemcpy(m->d_tri, m->trirec.data(), m->trirec.size() * sizeof(TriRec), cudaMemcpyHostToDevice),
+                     "cudaMemcpy H2D");
+  free_patch_plan(m);
+  if (!st) st = build_patch_plan(m);
+  if (!st) m->elem_type = type;
+  return st;
 }
 
 fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
@@ -645,19 +677,7 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_self_slot);
   cudaFree(m->d_line_fac);
   cudaFree(m->d_kry_work);
-  cudaFree(m->d_plan.t_begin);
-  cudaFree(m->d_plan.col_ptr);
-  cudaFree(m->d_plan.pair_ptr);
-  cudaFree(m->d_plan.contrib_ptr);
-  cudaFree(m->d_plan.cols);
-  cudaFree(m->d_plan.pairs);
-  cudaFree(m->d_plan.contrib);
-  cudaFree(m->d_plan.zero_cols);
-  cudaFree(m->d_plan.blob);
-  cudaFree(m->d_plan.blob_off);
-  cudaFree(m->d_plan.nedge);
-  cudaFree(m->d_plan.multi);
-  cudaFree(m->d_plan.partials);
+  free_patch_plan(m);
   cudaFree(m->d_stage_U);
   cudaFree(m->d_stage_R);
   cudaFree(m->d_stage_vals);

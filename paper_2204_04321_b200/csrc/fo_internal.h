@@ -135,6 +135,8 @@ struct fo_mesh_s {
   double* d_T = nullptr;           // per-wedge T* (NEXT-f3) or nullptr
   double A0fac = 0.0, QnR = 0.0;   // Arrhenius constants folded for the kernels
   int elem_type = FO_ELEM_WEDGE;   // NEXT-f4 (fo_element_tet.cuh)
+  std::vector<int32_t> tri_ccw;    // the caller's (CCW) corner order, kept while
+  std::vector<fo::TriRec> trirec_ccw;   // FO_ELEM_TET3 runs on global-id order
   // NEXT-f1 lateral margin term (fo_lateral.cu)
   bool lateral = false;
   int32_t n_lat_cols = 0, n_lat_faces = 0;
@@ -192,6 +194,7 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
 fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_vals,
                           void* stream);
 fo_status build_patch_plan(fo_mesh m);
+void free_patch_plan(fo_mesh m);
 // NEXT-f1 lateral margin term (fo_lateral.cu)
 fo_status build_lateral(fo_mesh m, int64_t n_tri_global, const int32_t* tri_global);
 fo_status launch_lateral(fo_mesh m, double* d_R, void* stream);

@@ -345,7 +345,6 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     const int* tp = reinterpret_cast<const int*>(tris + (t0 + tl));
     const int2 v01 = __ldg(reinterpret_cast<const int2*>(tp));
     tr.v[0] = v01.x; tr.v[1] = v01.y; tr.v[2] = __ldg(tp + 2);
-    if (TET) tr.pad[0] = uint8_t((__ldg(tp + 5) >> 8) & 0xff);   // NEXT-f4 split order
 #pragma unroll
     for (int i = 0; i < kD; ++i) D[i * TP + tl] = 0.0;
   }
@@ -368,7 +367,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       WedgeIn w;
       wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
       SmemCmp cmp{C, tl};
-      if constexpr (TET) tet3_element<N3>(w, tr.pad[0], kp.rg, kp.eps, kp.glen_n, sk);
+      if constexpr (TET) tet3_element<N3, true>(w, 0, kp.rg, kp.eps, kp.glen_n, sk);
       else wedge_element_v4<N3>(w, kp.rg, kp.eps, kp.glen_n, sk, cmp);
     }
     if (k == 0) bulk_wait(&plan_bar);

@@ -135,6 +135,15 @@ size_t plan_bytes(const PatchBuild& B) {
 
 }  // namespace
 
+void free_patch_plan(fo_mesh m) {
+  DevPatch& d = m->d_plan;
+  void* ptrs[] = {d.t_begin, d.col_ptr, d.pair_ptr, d.contrib_ptr, d.cols, d.pairs, d.contrib, d.zero_cols,
+                  d.blob, d.blob_off, d.nedge, d.multi, d.partials};
+  for (void* q : ptrs) cudaFree(q);
+  d = DevPatch();
+  m->plan = PatchPlan();
+}
+
 fo_status build_patch_plan(fo_mesh m) {
   PatchPlan& P = m->plan;
   P = PatchPlan();

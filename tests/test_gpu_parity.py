@@ -202,6 +202,14 @@ def test_tetrahedra_partitioned_and_rejections(torch_cuda, ora_mod):
         full.set_lateral(True)
     with pytest.raises(fo.FoError):
         full.set_scatter(1)
+    # back to wedges: the caller's corner order and plan are restored (bitwise)
+    full.set_element(0)
+    fresh = fo.Mesh.from_footprint(fp)
+    Uw = torch.tensor(fp.U, device="cuda")
+    Rw, Vw = full.jacobian(Uw)
+    Rw2, Vw2 = fresh.jacobian(Uw)
+    torch.cuda.synchronize()
+    assert torch.equal(Rw, Rw2) and torch.equal(Vw, Vw2)
 
 
 @pytest.mark.parametrize("L", [1, 2, 17])
