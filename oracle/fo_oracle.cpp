@@ -309,6 +309,8 @@ struct Mesh {
   std::vector<uint8_t> lateral;   /* [n_tri] boundary-edge bits (NEXT-f1) */
 };
 
+int validate_quads(const ora_mesh* m);
+
 int validate(const ora_mesh* m) {
   if (!m) return -1;
   if (m->n_vert < 0 || m->n_tri < 0 || m->n_layers < 1) return -1;
@@ -316,7 +318,8 @@ int validate(const ora_mesh* m) {
   if (!m->xy || !m->tri || !m->thickness || !m->surface || !m->beta) return -1;
   if (m->p.glen_n <= 0.0 || m->p.A <= 0.0 || m->p.eps_reg < 0.0) return -1;
   if (m->T_star && !(m->A0 > 0.0)) return -1;
-  if (m->elem_type != 0 && m->elem_type != 1) return -1;
+  if (m->elem_type != 0 && m->elem_type != 1 && m->elem_type != 2) return -1;
+  if (m->elem_type == 2) return validate_quads(m);
   const int L = m->n_layers;
   if (m->sigma) {
     if (m->sigma[0] != 0.0 || m->sigma[L] != 1.0) return -2;
@@ -411,7 +414,288 @@ int prepare(const ora_mesh* m, Mesh& M, int terms = 0) {
   int st = validate(m);
   if (st) return st;
   extrude(m, M);
-  if (terms & ORA_LATERAL) find_lateral(m, M);
+  if ((terms & ORA_LATERAL) && m->elem_type != 2) find_lateral(m, M);
+  return 0;
+}
+
+
+/* =================== NEXT-f4: 8-node trilinear hexahedra =================== */
+/* reading L23: quadrilateral footprint (CCW corners 0..3), element = the
+ * column segment between two levels, nodes 0..3 bottom (corner order), 4..7
+ * top; N_i = Q_c(xi, eta) f_l(zeta) with the bilinear Q_c at reference corners
+ * (-1,-1), (1,-1), (1,1), (-1,1); 2 x 2 x 2 Gauss points (+-1/sqrt 3, weight
+ * 1) with the generic 3x3 inverse; driving stress with the 3D basis gradient
+ * of nodal s; basal term with 2 x 2 Gauss on the bilinear bottom face, true 3D
+ * area element |X_xi x X_eta|, beta bilinear.  Jacobian by a 16-partial dual. */
+struct Dual16 {
+  double v;
+  double d[16];
+};
+inline Dual16 d16(double x) { Dual16 r; r.v = x; for (int i = 0; i < 16; ++i) r.d[i] = 0.0; return r; }
+inline Dual16 operator+(const Dual16& a, const Dual16& b) { Dual16 r; r.v = a.v + b.v; for (int i = 0; i < 16; ++i) r.d[i] = a.d[i] + b.d[i]; return r; }
+inline Dual16 operator*(const Dual16& a, const Dual16& b) { Dual16 r; r.v = a.v * b.v; for (int i = 0; i < 16; ++i) r.d[i] = a.d[i] * b.v + a.v * b.d[i]; return r; }
+inline Dual16 operator*(double a, const Dual16& b) { Dual16 r; r.v = a * b.v; for (int i = 0; i < 16; ++i) r.d[i] = a * b.d[i]; return r; }
+inline Dual16 operator*(const Dual16& b, double a) { return a * b; }
+inline Dual16 operator+(const Dual16& a, double b) { Dual16 r = a; r.v += b; return r; }
+inline Dual16& operator+=(Dual16& a, const Dual16& b) { a = a + b; return a; }
+inline Dual16 pow(const Dual16& a, double p) {
+  Dual16 r; r.v = std::pow(a.v, p);
+  double dp = p * std::pow(a.v, p - 1.0);
+  for (int i = 0; i < 16; ++i) r.d[i] = dp * a.d[i];
+  return r;
+}
+template <> inline Dual16 zero<Dual16>() { return d16(0.0); }
+template <> inline Dual16 promote<Dual16>(double x) { return d16(x); }
+
+const double kQxi[4] = {-1.0, 1.0, 1.0, -1.0}, kQeta[4] = {-1.0, -1.0, 1.0, 1.0};
+
+struct Geo8 {
+  double X[8][3];
+  double s[8];
+  double beta[4];
+  double A;
+  bool basal;
+  int64_t gdof[16];
+};
+
+int validate_quads(const ora_mesh* m) {
+  const int L = m->n_layers;
+  if (m->sigma) {
+    if (m->sigma[0] != 0.0 || m->sigma[L] != 1.0) return -2;
+    for (int k = 0; k < L; ++k) if (!(m->sigma[k + 1] > m->sigma[k])) return -2;
+  }
+  std::vector<char> used(m->n_vert, 0);
+  for (int64_t t = 0; t < m->n_tri; ++t) {
+    const int32_t* v = m->tri + 4 * t;
+    for (int j = 0; j < 4; ++j) if (v[j] < 0 || v[j] >= m->n_vert) return -2;
+    for (int j = 0; j < 4; ++j) {   /* convex, CCW: every corner turns left */
+      const int32_t a = v[(j + 3) % 4], b = v[j], c = v[(j + 1) % 4];
+      const double cr = (m->xy[2 * b] - m->xy[2 * a]) * (m->xy[2 * c + 1] - m->xy[2 * b + 1]) -
+                        (m->xy[2 * b + 1] - m->xy[2 * a + 1]) * (m->xy[2 * c] - m->xy[2 * b]);
+      if (!(cr > 0.0)) return -2;
+      used[b] = 1;
+    }
+  }
+  for (int64_t c = 0; c < m->n_vert; ++c) {
+    if (!used[c]) return -2;
+    if (!(m->thickness[c] >= m->p.H_min)) return -2;
+  }
+  return 0;
+}
+
+void hex_geo(const Mesh& M, int64_t t, int k, Geo8& e) {
+  const ora_mesh* m = M.m;
+  const int32_t* v = m->tri + 4 * t;
+  for (int l = 0; l < 2; ++l)
+    for (int j = 0; j < 4; ++j) {
+      const int i = j + 4 * l;
+      const int64_t node = int64_t(v[j]) * (M.L + 1) + k + l;
+      e.X[i][0] = m->xy[2 * v[j]];
+      e.X[i][1] = m->xy[2 * v[j] + 1];
+      e.X[i][2] = M.z[node];
+      e.s[i] = m->surface[v[j]];
+      e.gdof[2 * i] = 2 * node;
+      e.gdof[2 * i + 1] = 2 * node + 1;
+    }
+  for (int j = 0; j < 4; ++j) e.beta[j] = M.beta[v[j]];
+  if (m->T_star)
+    e.A = m->A0 * std::exp(-m->Q_act / (kGasR * m->T_star[t * M.L + k]));
+  else
+    e.A = m->A_elem ? m->A_elem[t * M.L + k] : m->p.A;
+  e.basal = (k == 0);
+}
+
+/* N, dN/d(xi,eta,zeta) of the 8 nodes; physical gradients by the generic inverse */
+double hex_basis(const Geo8& e, double xi, double eta, double zeta, double N[8], double G[8][3]) {
+  double dN[8][3];
+  for (int l = 0; l < 2; ++l)
+    for (int j = 0; j < 4; ++j) {
+      const int i = j + 4 * l;
+      const double fq = 0.25 * (1.0 + kQxi[j] * xi) * (1.0 + kQeta[j] * eta);
+      const double fz = l == 0 ? 0.5 * (1.0 - zeta) : 0.5 * (1.0 + zeta);
+      N[i] = fq * fz;
+      dN[i][0] = 0.25 * kQxi[j] * (1.0 + kQeta[j] * eta) * fz;
+      dN[i][1] = 0.25 * kQeta[j] * (1.0 + kQxi[j] * xi) * fz;
+      dN[i][2] = fq * (l == 0 ? -0.5 : 0.5);
+    }
+  double Jm[3][3] = {{0}};
+  for (int i = 0; i < 8; ++i)
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Jm[r][c] += e.X[i][r] * dN[i][c];
+  const double det = Jm[0][0] * (Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1]) -
+                     Jm[0][1] * (Jm[1][0] * Jm[2][2] - Jm[1][2] * Jm[2][0]) +
+                     Jm[0][2] * (Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0]);
+  double inv[3][3];
+  inv[0][0] = (Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1]) / det;
+  inv[0][1] = (Jm[0][2] * Jm[2][1] - Jm[0][1] * Jm[2][2]) / det;
+  inv[0][2] = (Jm[0][1] * Jm[1][2] - Jm[0][2] * Jm[1][1]) / det;
+  inv[1][0] = (Jm[1][2] * Jm[2][0] - Jm[1][0] * Jm[2][2]) / det;
+  inv[1][1] = (Jm[0][0] * Jm[2][2] - Jm[0][2] * Jm[2][0]) / det;
+  inv[1][2] = (Jm[0][2] * Jm[1][0] - Jm[0][0] * Jm[1][2]) / det;
+  inv[2][0] = (Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0]) / det;
+  inv[2][1] = (Jm[0][1] * Jm[2][0] - Jm[0][0] * Jm[2][1]) / det;
+  inv[2][2] = (Jm[0][0] * Jm[1][1] - Jm[0][1] * Jm[1][0]) / det;
+  for (int i = 0; i < 8; ++i)
+    for (int r = 0; r < 3; ++r) {
+      double acc = 0.0;
+      for (int c = 0; c < 3; ++c) acc += inv[c][r] * dN[i][c];
+      G[i][r] = acc;
+    }
+  return det;
+}
+
+template <class T>
+void element_hex(const Geo8& e, const ora_params& p, int terms, const T Ul[16], T r[16], T* pi) {
+  for (int j = 0; j < 16; ++j) r[j] = zero<T>();
+  T energy = zero<T>();
+  const double n = p.glen_n;
+  const double Afac = std::pow(e.A, -1.0 / n);
+  const double rg = p.rho * p.g;
+  const double gz = 1.0 / std::sqrt(3.0);
+  for (int qx = 0; qx < 2; ++qx)
+    for (int qy = 0; qy < 2; ++qy)
+      for (int qz = 0; qz < 2; ++qz) {
+        double N[8], G[8][3];
+        const double det = hex_basis(e, qx ? gz : -gz, qy ? gz : -gz, qz ? gz : -gz, N, G);
+        const double W = det;   /* Gauss weights 1 x 1 x 1 */
+        T ux = zero<T>(), uy = zero<T>(), uz = zero<T>(), vx = zero<T>(), vy = zero<T>(), vz = zero<T>();
+        T u = zero<T>(), v = zero<T>();
+        for (int i = 0; i < 8; ++i) {
+          ux += Ul[2 * i] * G[i][0]; uy += Ul[2 * i] * G[i][1]; uz += Ul[2 * i] * G[i][2];
+          vx += Ul[2 * i + 1] * G[i][0]; vy += Ul[2 * i + 1] * G[i][1]; vz += Ul[2 * i + 1] * G[i][2];
+          u += Ul[2 * i] * N[i]; v += Ul[2 * i + 1] * N[i];
+        }
+        if (terms & ORA_VISC) {
+          T exx = ux, eyy = vy, exy = 0.5 * (uy + vx), exz = 0.5 * uz, eyz = 0.5 * vz;
+          T q = exx * exx + eyy * eyy + exx * eyy + exy * exy + exz * exz + eyz * eyz;
+          T qe = q + p.eps_reg;
+          T two_mu = Afac * pow(qe, (1.0 - n) / (2.0 * n));
+          T e1[3] = {2.0 * exx + eyy, exy, exz};
+          T e2[3] = {exy, exx + 2.0 * eyy, eyz};
+          for (int i = 0; i < 8; ++i) {
+            T g1 = e1[0] * G[i][0] + e1[1] * G[i][1] + e1[2] * G[i][2];
+            T g2 = e2[0] * G[i][0] + e2[1] * G[i][1] + e2[2] * G[i][2];
+            r[2 * i] += (W * two_mu) * g1;
+            r[2 * i + 1] += (W * two_mu) * g2;
+          }
+          energy += (W * (2.0 * n / (n + 1.0)) * Afac) * pow(qe, (n + 1.0) / (2.0 * n));
+        }
+        if (terms & ORA_BODY) {
+          double sx = 0.0, sy = 0.0;
+          for (int i = 0; i < 8; ++i) { sx += e.s[i] * G[i][0]; sy += e.s[i] * G[i][1]; }
+          for (int i = 0; i < 8; ++i) {
+            r[2 * i] += promote<T>(W * rg * sx * N[i]);
+            r[2 * i + 1] += promote<T>(W * rg * sy * N[i]);
+          }
+          energy += (W * rg * sx) * u + (W * rg * sy) * v;
+        }
+      }
+  if ((terms & ORA_BASAL) && e.basal) {
+    for (int qx = 0; qx < 2; ++qx)
+      for (int qy = 0; qy < 2; ++qy) {
+        const double xi = qx ? gz : -gz, eta = qy ? gz : -gz;
+        double Q[4], tx[3] = {0, 0, 0}, ty[3] = {0, 0, 0};
+        for (int j = 0; j < 4; ++j) {
+          Q[j] = 0.25 * (1.0 + kQxi[j] * xi) * (1.0 + kQeta[j] * eta);
+          const double dxi = 0.25 * kQxi[j] * (1.0 + kQeta[j] * eta);
+          const double deta = 0.25 * kQeta[j] * (1.0 + kQxi[j] * xi);
+          for (int r3 = 0; r3 < 3; ++r3) { tx[r3] += dxi * e.X[j][r3]; ty[r3] += deta * e.X[j][r3]; }
+        }
+        const double cx = tx[1] * ty[2] - tx[2] * ty[1], cy = tx[2] * ty[0] - tx[0] * ty[2],
+                     cz = tx[0] * ty[1] - tx[1] * ty[0];
+        const double w = std::sqrt(cx * cx + cy * cy + cz * cz);   /* weight 1 x 1 */
+        double b = 0.0;
+        for (int j = 0; j < 4; ++j) b += Q[j] * e.beta[j];
+        T u = zero<T>(), v = zero<T>();
+        for (int j = 0; j < 4; ++j) { u += Q[j] * Ul[2 * j]; v += Q[j] * Ul[2 * j + 1]; }
+        for (int j = 0; j < 4; ++j) {
+          r[2 * j] += (w * b * Q[j]) * u;
+          r[2 * j + 1] += (w * b * Q[j]) * v;
+        }
+        energy += (0.5 * w * b) * (u * u + v * v);
+      }
+  }
+  if (pi) *pi = energy;
+}
+
+/* hexahedral versions of the drivers (elem_type 2) */
+int graph_hex(const ora_mesh* m, const Mesh& M, int64_t* row_ptr, int32_t* col_idx, int64_t* nnz) {
+  std::vector<std::vector<int64_t>> rows(M.n_dof);
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int k = 0; k < M.L; ++k) {
+      Geo8 e;
+      hex_geo(M, t, k, e);
+      for (int p = 0; p < 16; ++p)
+        for (int q = 0; q < 16; ++q) rows[e.gdof[p]].push_back(e.gdof[q]);
+    }
+  int64_t total = 0;
+  for (int64_t r = 0; r < M.n_dof; ++r) {
+    std::sort(rows[r].begin(), rows[r].end());
+    rows[r].erase(std::unique(rows[r].begin(), rows[r].end()), rows[r].end());
+    total += int64_t(rows[r].size());
+  }
+  if (nnz) *nnz = total;
+  if (row_ptr) {
+    row_ptr[0] = 0;
+    for (int64_t r = 0; r < M.n_dof; ++r) row_ptr[r + 1] = row_ptr[r] + int64_t(rows[r].size());
+  }
+  if (col_idx) {
+    int64_t pos = 0;
+    for (int64_t r = 0; r < M.n_dof; ++r)
+      for (int64_t c : rows[r]) col_idx[pos++] = int32_t(c);
+  }
+  return 0;
+}
+
+int residual_hex(const ora_mesh* m, const Mesh& M, int terms, const double* U, double* R, double* Mabs,
+                 double* Pi, int64_t dof) {
+  double pi_total = 0.0;
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int k = 0; k < M.L; ++k) {
+      Geo8 e;
+      hex_geo(M, t, k, e);
+      if (dof >= 0) {
+        bool touches = false;
+        for (int j = 0; j < 16 && !touches; ++j) touches = (e.gdof[j] == dof);
+        if (!touches) continue;
+      }
+      double Ul[16], r[16], pi;
+      for (int j = 0; j < 16; ++j) Ul[j] = U[e.gdof[j]];
+      element_hex<double>(e, m->p, terms, Ul, r, &pi);
+      for (int j = 0; j < 16; ++j) {
+        if (R) R[e.gdof[j]] += r[j];
+        if (Mabs) Mabs[e.gdof[j]] += std::fabs(r[j]);
+      }
+      pi_total += pi;
+    }
+  if (Pi) *Pi = pi_total;
+  return 0;
+}
+
+int jacobian_hex(const ora_mesh* m, const Mesh& M, int terms, const double* U, const int64_t* row_ptr,
+                 const int32_t* col_idx, double* R, double* vals) {
+  for (int64_t t = 0; t < m->n_tri; ++t)
+    for (int k = 0; k < M.L; ++k) {
+      Geo8 e;
+      hex_geo(M, t, k, e);
+      Dual16 Ul[16], r[16];
+      for (int j = 0; j < 16; ++j) {
+        Ul[j] = d16(U[e.gdof[j]]);
+        Ul[j].d[j] = 1.0;
+      }
+      element_hex<Dual16>(e, m->p, terms, Ul, r, nullptr);
+      for (int p = 0; p < 16; ++p) {
+        const int64_t row = e.gdof[p];
+        if (R) R[row] += r[p].v;
+        const int32_t* b = col_idx + row_ptr[row];
+        const int32_t* end = col_idx + row_ptr[row + 1];
+        for (int q = 0; q < 16; ++q) {
+          const int32_t* it = std::lower_bound(b, end, int32_t(e.gdof[q]));
+          if (it == end || *it != e.gdof[q]) return -3;
+          vals[it - col_idx] += r[p].d[q];
+        }
+      }
+    }
   return 0;
 }
 
@@ -425,6 +709,7 @@ int ora_graph(const ora_mesh* m, int64_t* row_ptr, int32_t* col_idx, int64_t* nn
   Mesh M;
   int st = prepare(m, M);
   if (st) return st;
+  if (m->elem_type == 2) return graph_hex(m, M, row_ptr, col_idx, nnz);
   /* brute force: every DOF pair of every wedge, then sort + unique per row */
   std::vector<std::vector<int64_t>> rows(M.n_dof);
   for (int64_t t = 0; t < m->n_tri; ++t)
@@ -459,6 +744,7 @@ int ora_residual(const ora_mesh* m, int terms, const double* U, double* R, doubl
   if (st) return st;
   if (R) std::memset(R, 0, sizeof(double) * M.n_dof);
   if (Mabs) std::memset(Mabs, 0, sizeof(double) * M.n_dof);
+  if (m->elem_type == 2) return residual_hex(m, M, terms, U, R, Mabs, Pi, -1);
   double pi_total = 0.0;
   for (int64_t t = 0; t < m->n_tri; ++t)
     for (int k = 0; k < M.L; ++k) {
@@ -485,6 +771,7 @@ int ora_jacobian(const ora_mesh* m, int terms, const double* U, const int64_t* r
   if (!row_ptr || !col_idx || !vals) return -1;
   if (R) std::memset(R, 0, sizeof(double) * M.n_dof);
   std::memset(vals, 0, sizeof(double) * row_ptr[M.n_dof]);
+  if (m->elem_type == 2) return jacobian_hex(m, M, terms, U, row_ptr, col_idx, R, vals);
   for (int64_t t = 0; t < m->n_tri; ++t)
     for (int k = 0; k < M.L; ++k) {
       Geo e;
@@ -514,6 +801,7 @@ int ora_energy(const ora_mesh* m, int terms, const double* U, int64_t dof, doubl
   Mesh M;
   int st = prepare(m, M, terms);
   if (st) return st;
+  if (m->elem_type == 2) return residual_hex(m, M, terms, U, nullptr, nullptr, Pi, dof);
   double total = 0.0;
   for (int64_t t = 0; t < m->n_tri; ++t)
     for (int k = 0; k < M.L; ++k) {
@@ -536,7 +824,7 @@ int ora_element(const ora_mesh* m, int terms, const double* U, int64_t t, int32_
   Mesh M;
   int st = prepare(m, M, terms);
   if (st) return st;
-  if (t < 0 || t >= m->n_tri || k < 0 || k >= M.L) return -1;
+  if (t < 0 || t >= m->n_tri || k < 0 || k >= M.L || m->elem_type == 2) return -1;
   Geo e;
   wedge_geo(M, t, k, e);
   Dual Ul[12], rr[12];

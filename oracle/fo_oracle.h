@@ -57,8 +57,10 @@ typedef struct {
   const double* T_star;     /* [n_tri*L] K, or NULL */
   double A0;                /* Pa^-n a^-1 */
   double Q_act;             /* J mol^-1 */
-  /* NEXT-f4: 0 = 6-node wedge (reading L5), 1 = three 4-node P1
-   * tetrahedra per prism, split by global vertex id (reading L22) */
+  /* NEXT-f4: 0 = 6-node wedge (reading L5), 1 = three 4-node
+   * P1 tetrahedra per prism, split by global vertex id (reading L22), 2 = the
+   * footprint is QUADRILATERAL (tri holds n_tri x 4 CCW corners) and every
+   * layer element an 8-node trilinear hexahedron (reading L23) */
   int32_t elem_type;
 } ora_mesh;
 

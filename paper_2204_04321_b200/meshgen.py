@@ -85,7 +85,8 @@ class Footprint:
     A_elem: np.ndarray | None = None
     T_star: np.ndarray | None = None    # NEXT-f3: per-wedge temperature (K)
     arrhenius: dict | None = None       # {"A0": Pa^-n a^-1, "Q": J/mol}
-    elem_type: int = 0                  # NEXT-f4: 0 wedge, 1 three P1 tetrahedra per prism
+    elem_type: int = 0                  # NEXT-f4: 0 wedge, 1 three P1 tetrahedra per prism,
+                                        # 2 quadrilateral footprint (tri = [n, 4]) and hexahedra
 
     @property
     def n_vert(self) -> int:
@@ -217,6 +218,21 @@ def slab(nx: int = 20, n_layers: int = 5, length: float = 80e3, H0: float = 1000
     else:
         U = np.zeros(2 * nv * (n_layers + 1))
     return Footprint("slab", xy, fp.tri.copy(), sigma, H, s, None, beta, U, params)
+
+
+def to_quads(fp: Footprint, nx: int) -> Footprint:
+    """NEXT-f4 hexahedral workload: the (nx+1)^2 grid of an ismip_hom_a / slab
+    footprint as nx^2 CCW quadrilaterals (v(i,j), v(i+1,j), v(i+1,j+1), v(i,j+1)),
+    vertex id i*(nx+1)+j; fields and U unchanged."""
+    q = []
+    for i in range(nx):
+        for j in range(nx):
+            q.append((i * (nx + 1) + j, (i + 1) * (nx + 1) + j, (i + 1) * (nx + 1) + j + 1, i * (nx + 1) + j + 1))
+    out = Footprint(fp.name + "-quads", fp.xy.copy(), np.array(q, dtype=np.int32), fp.sigma.copy(),
+                    fp.thickness.copy(), fp.surface.copy(), None if fp.bed is None else fp.bed.copy(),
+                    fp.beta.copy(), fp.U.copy(), dict(fp.params))
+    out.elem_type = 2
+    return out
 
 
 # --------------------------------------------------------------------------

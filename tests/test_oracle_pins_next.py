@@ -260,3 +260,91 @@ def test_f4_tet_structural_zeros(ora_mod):
             blk = J[2 * nd(a, 1):2 * nd(a, 1) + 2, 2 * nd(c, 1):2 * nd(c, 1) + 2]
             nonzero_pairs += int(np.any(blk != 0.0))
     assert zero_pairs > 0 and nonzero_pairs == len(fp.tri) * fp.n_layers
+
+
+# ---------------------------------------------------------------- f4 hexahedra
+# quadrilateral footprint, 8-node trilinear hexahedra (reading L23)
+@pytest.mark.parametrize("n_glen", [1.0, 3.0])
+def test_f4_hex_patch_test(ora_mod, n_glen):
+    """Linear U, flat s, beta = 0 on distorted quad columns: interior residuals
+    vanish (isoparametric trilinear elements reproduce linear fields)."""
+    nx = 5
+    fp = mg.to_quads(mg.slab(nx=nx, n_layers=4, distort=0.2, params=dict(glen_n=n_glen)), nx)
+    o = ora_mod.Oracle(fp)
+    L1 = fp.n_layers + 1
+    base = fp.surface - fp.thickness
+    z = (base[:, None] + fp.sigma[None, :] * fp.thickness[:, None]).reshape(-1)
+    x = np.repeat(fp.xy[:, 0], L1)
+    y = np.repeat(fp.xy[:, 1], L1)
+    U = np.zeros(o.n_dof)
+    U[0::2] = 3.0 + 2e-3 * x - 1e-3 * y + 0.05 * z
+    U[1::2] = -1.0 + 1e-3 * x + 4e-3 * y - 0.02 * z
+    R, M, _ = o.residual(U, terms=ora_mod.VISC)
+    col = np.arange(fp.n_vert)
+    edge = np.unique(np.concatenate([np.arange(nx + 1), np.arange(nx * (nx + 1), (nx + 1) ** 2),
+                                     np.arange(0, (nx + 1) ** 2, nx + 1), np.arange(nx, (nx + 1) ** 2, nx + 1)]))
+    k = np.arange(L1)
+    node_int = (~np.isin(col, edge)[:, None] & (k[None, :] > 0) & (k[None, :] < fp.n_layers)).reshape(-1)
+    dof_int = np.repeat(node_int, 2)
+    assert np.abs(R[dof_int]).max() <= 1e-12 * np.abs(M).max()
+    assert np.abs(R[~dof_int]).max() > 1e-6 * np.abs(M).max()
+
+
+def test_f4_hex_driving_stress_and_basal_totals(ora_mod):
+    """Rectangular hexes with a planar surface: sum_i R_u(U=0) = rho g s_x x
+    (column volume), and with constant U and beta: sum_i R_u = beta u (bed area)."""
+    nx = 4
+    fp = mg.to_quads(mg.slab(nx=nx, n_layers=3, H0=800.0), nx)
+    fp.surface = fp.surface + 1e-3 * fp.xy[:, 0] - 2e-3 * fp.xy[:, 1]
+    fp.thickness = 800.0 + 1e-3 * fp.xy[:, 0]
+    o = ora_mod.Oracle(fp)
+    R, _, _ = o.residual(np.zeros(o.n_dof), terms=ora_mod.BODY)
+    Lx = fp.xy[:, 0].max() - fp.xy[:, 0].min()
+    vol = Lx * Lx * (800.0 + 1e-3 * Lx / 2.0)   # H linear in x: mean over the square
+    assert abs(R[0::2].sum() - 910.0 * 9.81 * 1e-3 * vol) <= 1e-12 * abs(910.0 * 9.81 * 1e-3 * vol)
+    assert abs(R[1::2].sum() - 910.0 * 9.81 * (-2e-3) * vol) <= 1e-12 * abs(910.0 * 9.81 * 2e-3 * vol)
+    fp.beta = np.full(fp.n_vert, 700.0)
+    U = np.zeros(o.n_dof)
+    U[0::2], U[1::2] = 3.0, -2.0
+    o = ora_mod.Oracle(fp)
+    Rb = o.residual(U, terms=ora_mod.BASAL)[0]
+    # bed: planar (s - H linear), area = Lx^2 sqrt(1 + |grad b|^2)
+    gb = np.array([1e-3 - 1e-3, -2e-3])
+    area = Lx * Lx * np.sqrt(1.0 + gb @ gb)
+    assert abs(Rb[0::2].sum() - 700.0 * 3.0 * area) <= 1e-12 * 700.0 * 3.0 * area
+    assert abs(Rb[1::2].sum() + 700.0 * 2.0 * area) <= 1e-12 * 700.0 * 2.0 * area
+
+
+def test_f4_hex_nullspace_symmetry_fd(ora_mod):
+    nx = 3
+    fp = mg.to_quads(mg.slab(nx=nx, n_layers=2, distort=0.15), nx)
+    fp.U = fp.U * (1.0 + 0.1 * np.sin(np.arange(fp.U.size)))
+    o = ora_mod.Oracle(fp)
+    J = o.dense_jacobian(fp.U, terms=ora_mod.VISC)
+    L1 = fp.n_layers + 1
+    x = np.repeat(fp.xy[:, 0], L1)
+    y = np.repeat(fp.xy[:, 1], L1)
+    for w in (np.tile([1.0, 0.0], o.n_dof // 2), np.tile([0.0, 1.0], o.n_dof // 2),
+              np.stack([-y, x], axis=1).reshape(-1)):
+        assert np.abs(J @ w).max() <= 1e-12 * np.abs(J).max() * np.abs(w).max()
+    Jf = o.dense_jacobian(fp.U)
+    assert np.abs(Jf - Jf.T).max() <= 1e-14 * np.abs(Jf).max()
+    U = fp.U
+    R = o.residual(U)[0]
+    for j in np.linspace(0, o.n_dof - 1, 10).astype(int):
+        h = 1e-6 * max(1.0, abs(U[j]))
+        Up, Um = U.copy(), U.copy()
+        Up[j] += h
+        Um[j] -= h
+        fd = (o.residual(Up)[0] - o.residual(Um)[0]) / (2 * h)
+        assert np.abs(Jf[:, j] - fd).max() <= 1e-6 * np.abs(Jf[:, j]).max()
+        he = 1e-4 * max(1.0, abs(U[j]))
+        Up, Um = U.copy(), U.copy()
+        Up[j] += he
+        Um[j] -= he
+        fde = (o.energy(Up, dof=j) - o.energy(Um, dof=j)) / (2 * he)
+        assert abs(fde - R[j]) <= 1e-6 * np.abs(R).max()
+    # graph: every column couples to its 8 grid neighbours and itself
+    rp, col = o.graph()
+    assert rp[-1] == 4 * (3 * fp.n_layers + 1) * sum(
+        len({int(v) for q in fp.tri if c in q for v in q}) for c in range(fp.n_vert))
