@@ -120,6 +120,21 @@ FO_API fo_status fo_mesh_create_part(const fo_params* p, int64_t n_vert, const d
  * FO_EINVAL: mesh NULL, A0 <= 0 or some T* <= 0.  Synchronous. */
 FO_API fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, double Q);
 
+/* NEXT-f4: hexahedral mesh from a QUADRILATERAL footprint:
+ * quad[n_quad][4] 0-based CCW corners of convex quads (FO_EMESH otherwise),
+ * every other argument as fo_mesh_create (A_elem[n_quad*L]).  Each layer
+ * element is an 8-node trilinear hexahedron (reading L23: 2x2x2 Gauss,
+ * isoparametric, exact Jacobian; basal term with 2x2 Gauss on the bilinear
+ * bottom face).  Graph, SpMV, line preconditioner, A(T) apply unchanged; the
+ * scatter is coloured (quads sharing a corner never run concurrently; a fixed
+ * launch order makes it deterministic).  Single-domain; no lateral term, no
+ * fo_set_element / atomic scatter.  Synchronous. */
+FO_API fo_status fo_mesh_create_quad(const fo_params* p, int64_t n_vert, const double* xy,
+                                     int64_t n_quad, const int32_t* quad, int32_t n_layers,
+                                     const double* sigma, const double* thickness,
+                                     const double* surface, const double* bed, const double* beta,
+                                     const double* A_elem, int device, fo_mesh* out);
+
 /* Contiguous partition of the (Hilbert-ordered) triangle list:
  * part_of_tri[t] = floor(t * n_parts / n_tri).  Host only. */
 FO_API fo_status fo_partition(int64_t n_tri, int32_t n_parts, int32_t* part_of_tri);

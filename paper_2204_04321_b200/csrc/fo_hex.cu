@@ -1,0 +1,450 @@
+// fo_hex.cu -- NEXT-f4: quadrilateral footprints with 8-node trilinear
+// hexahedra (the Antarctic hex meshes; reading L23).
+//
+// Same weak form, residual and exact Jacobian as the wedge path,
+// per hexahedron: 2 x 2 x 2 Gauss points, trilinear basis N_i = Q_c(xi, eta)
+// f_l(zeta) with the physical gradients from the generic 3x3 inverse of the
+// isoparametric map (the footprint map is bilinear, so nothing separates as for
+// the wedge), J = sum_q w_q [2 mu_q H_q - d_q g_q g_q^T] accumulated in the
+// thread's shared-memory block (136 upper-triangle values + 16 residual).
+// Basal term: 2 x 2 Gauss on the bilinear bottom face, true 3D area element.
+//
+// Scatter: COLOURED.  Quads are greedily coloured so that no two quads of a
+// colour share a corner; colour c, layer parity l launches touch disjoint node
+// sets, so each thread adds its block into the (zeroed) CSR values and residual
+// with plain read-modify-write, in a fixed launch order: deterministic.  CSR
+// positions come from the column structure (QuadRec slots), col_idx is not read.
+// The graph, SpMV and line preconditioner of the wedge path apply unchanged
+// (they only see columns and coupling lists).  Single-domain meshes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "fo_internal.h"
+#include "fo_kernels.cuh"
+
+namespace fo {
+
+namespace {
+
+constexpr int kHexThreads = 64;
+constexpr int kHexAcc = 136 + 16;   // upper triangle of the 16 x 16 block + residual
+
+__device__ __forceinline__ int pk16(int p, int q) {   // packed upper triangle, p <= q
+  return p * 16 - (p * (p - 1)) / 2 + (q - p);
+}
+
+template <bool NEED_J, bool N3>
+__global__ void __launch_bounds__(kHexThreads)
+hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, const int32_t* __restrict__ ids,
+           int n_ids, int kpar, const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
+           const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
+  extern __shared__ double hsm[];
+  const int L = kp.L;
+  const int nk = (L - kpar + 1) / 2;   // layers k = kpar, kpar + 2, ...
+  const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= int64_t(n_ids) * nk) return;
+  const int qi = __ldg(ids + item / nk);
+  const int k = kpar + 2 * int(item % nk);
+  double* acc = hsm + threadIdx.x;   // acc[i * kHexThreads]
+#define ACC(i) acc[(i) * kHexThreads]
+  for (int i = 0; i < kHexAcc; ++i) ACC(i) = 0.0;
+  const QuadRec qr = quads[qi];
+  double X[8], Y[8], Z[8], S[8], Uu[8], Uv[8], B[4];
+  int64_t cs[4];
+  int nc[4];
+  const double s0 = __ldg(sigma + k), s1 = __ldg(sigma + k + 1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const ColRec c = col[qr.v[j]];
+    cs[j] = c.cs_n >> 8;
+    nc[j] = int(c.cs_n & 255);
+    X[j] = X[j + 4] = c.x;
+    Y[j] = Y[j + 4] = c.y;
+    Z[j] = fma(s0, c.H, c.base);
+    Z[j + 4] = fma(s1, c.H, c.base);
+    S[j] = S[j + 4] = c.base + c.H;
+    B[j] = c.beta;
+    const int64_t node = int64_t(qr.v[j]) * (L + 1) + k;
+    const double2 ub = __ldg(reinterpret_cast<const double2*>(U) + node);
+    const double2 ut = __ldg(reinterpret_cast<const double2*>(U) + node + 1);
+    Uu[j] = ub.x; Uv[j] = ub.y; Uu[j + 4] = ut.x; Uv[j + 4] = ut.y;
+  }
+  const double Afac = wedge_afac(kp, Aw, qi, k);
+  const double ex1 = (1.0 - kp.glen_n) / (2.0 * kp.glen_n), kap = (kp.glen_n - 1.0) / (2.0 * kp.glen_n);
+  constexpr double gz = 0.57735026918962576451;
+  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+#pragma unroll 1
+  for (int qp = 0; qp < 8; ++qp) {
+    const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
+    double N[8], dN[8][3];
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = j + 4 * l;
+        const double fq = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+        const double fz = l == 0 ? 0.5 * (1.0 - zeta) : 0.5 * (1.0 + zeta);
+        N[i] = fq * fz;
+        dN[i][0] = 0.25 * cxi[j] * (1.0 + ceta[j] * eta) * fz;
+        dN[i][1] = 0.25 * ceta[j] * (1.0 + cxi[j] * xi) * fz;
+        dN[i][2] = fq * (l == 0 ? -0.5 : 0.5);
+      }
+    double J00 = 0, J01 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0, J20 = 0, J21 = 0, J22 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      J00 = fma(X[i], dN[i][0], J00); J01 = fma(X[i], dN[i][1], J01); J02 = fma(X[i], dN[i][2], J02);
+      J10 = fma(Y[i], dN[i][0], J10); J11 = fma(Y[i], dN[i][1], J11); J12 = fma(Y[i], dN[i][2], J12);
+      J20 = fma(Z[i], dN[i][0], J20); J21 = fma(Z[i], dN[i][1], J21); J22 = fma(Z[i], dN[i][2], J22);
+    }
+    const double c00 = J11 * J22 - J12 * J21, c01 = J12 * J20 - J10 * J22, c02 = J10 * J21 - J11 * J20;
+    const double det = J00 * c00 + J01 * c01 + J02 * c02;
+    const double id = 1.0 / det;
+    // inverse (row r = d(xi_r)/d(x)): inv[c][r] in the oracle's notation
+    const double i00 = c00 * id, i01 = (J02 * J21 - J01 * J22) * id, i02 = (J01 * J12 - J02 * J11) * id;
+    const double i10 = c01 * id, i11 = (J00 * J22 - J02 * J20) * id, i12 = (J02 * J10 - J00 * J12) * id;
+    const double i20 = c02 * id, i21 = (J01 * J20 - J00 * J21) * id, i22 = (J00 * J11 - J01 * J10) * id;
+    double G[8][3];
+    double ux = 0, uy = 0, uz = 0, vx = 0, vy = 0, vz = 0, sx = 0, sy = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      G[i][0] = i00 * dN[i][0] + i10 * dN[i][1] + i20 * dN[i][2];
+      G[i][1] = i01 * dN[i][0] + i11 * dN[i][1] + i21 * dN[i][2];
+      G[i][2] = i02 * dN[i][0] + i12 * dN[i][1] + i22 * dN[i][2];
+      ux = fma(Uu[i], G[i][0], ux); uy = fma(Uu[i], G[i][1], uy); uz = fma(Uu[i], G[i][2], uz);
+      vx = fma(Uv[i], G[i][0], vx); vy = fma(Uv[i], G[i][1], vy); vz = fma(Uv[i], G[i][2], vz);
+      sx = fma(S[i], G[i][0], sx); sy = fma(S[i], G[i][1], sy);
+    }
+    const double W = det;   // Gauss weights 1
+    const double exy = 0.5 * (uy + vx), exz = 0.5 * uz, eyz = 0.5 * vz;
+    const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
+    const double qe = qq + kp.eps;
+    double c, d;
+    if (N3) {
+      const double y = rcbrt(qe);
+      c = W * Afac * y;
+      d = c * (y * y * y) * (1.0 / 3.0);
+    } else {
+      c = W * Afac * pow(qe, ex1);
+      d = c * kap / qe;
+    }
+    const double e1x = 2.0 * ux + vy, e2y = ux + 2.0 * vy;
+    double g[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      g[2 * i] = fma(e1x, G[i][0], fma(exy, G[i][1], exz * G[i][2]));
+      g[2 * i + 1] = fma(exy, G[i][0], fma(e2y, G[i][1], eyz * G[i][2]));
+    }
+    const double bw = W * kp.rg;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      ACC(136 + 2 * i) += fma(c, g[2 * i], bw * sx * N[i]);
+      ACC(136 + 2 * i + 1) += fma(c, g[2 * i + 1], bw * sy * N[i]);
+    }
+    if (NEED_J) {
+#pragma unroll 1
+      for (int i = 0; i < 8; ++i) {
+#pragma unroll
+        for (int i2 = 0; i2 < 8; ++i2) {
+          if (i2 < i) continue;
+          const double xx = G[i][0] * G[i2][0], yy = G[i][1] * G[i2][1], zz = G[i][2] * G[i2][2];
+          const double xy = G[i][0] * G[i2][1], yx = G[i][1] * G[i2][0];
+          const double huu = fma(2.0, xx, 0.5 * (yy + zz)), hvv = fma(2.0, yy, 0.5 * (xx + zz));
+          const double huv = fma(0.5, yx, xy), hvu = fma(0.5, xy, yx);
+          const int p = 2 * i, p2 = 2 * i2;
+          ACC(pk16(p, p2)) += fma(c, huu, -d * g[p] * g[p2]);
+          ACC(pk16(p, p2 + 1)) += fma(c, huv, -d * g[p] * g[p2 + 1]);
+          if (i2 > i) ACC(pk16(p + 1, p2)) += fma(c, hvu, -d * g[p + 1] * g[p2]);
+          ACC(pk16(p + 1, p2 + 1)) += fma(c, hvv, -d * g[p + 1] * g[p2 + 1]);
+        }
+      }
+    }
+  }
+  if (k == 0) {   // basal Robin term on the bilinear bottom face
+#pragma unroll 1
+    for (int qp = 0; qp < 4; ++qp) {
+      const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz;
+      double Q[4], tx0 = 0, tx1 = 0, tx2 = 0, ty0 = 0, ty1 = 0, ty2 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        Q[j] = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+        const double dxi = 0.25 * cxi[j] * (1.0 + ceta[j] * eta), deta = 0.25 * ceta[j] * (1.0 + cxi[j] * xi);
+        tx0 = fma(dxi, X[j], tx0); tx1 = fma(dxi, Y[j], tx1); tx2 = fma(dxi, Z[j], tx2);
+        ty0 = fma(deta, X[j], ty0); ty1 = fma(deta, Y[j], ty1); ty2 = fma(deta, Z[j], ty2);
+      }
+      const double cx = tx1 * ty2 - tx2 * ty1, cy = tx2 * ty0 - tx0 * ty2, cz = tx0 * ty1 - tx1 * ty0;
+      const double w = sqrt(cx * cx + cy * cy + cz * cz);
+      const double b = w * (Q[0] * B[0] + Q[1] * B[1] + Q[2] * B[2] + Q[3] * B[3]);
+      const double u = Q[0] * Uu[0] + Q[1] * Uu[1] + Q[2] * Uu[2] + Q[3] * Uu[3];
+      const double v = Q[0] * Uv[0] + Q[1] * Uv[1] + Q[2] * Uv[2] + Q[3] * Uv[3];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ACC(136 + 2 * j) += b * Q[j] * u;
+        ACC(136 + 2 * j + 1) += b * Q[j] * v;
+        if (NEED_J) {
+#pragma unroll
+          for (int j2 = j; j2 < 4; ++j2) {
+            ACC(pk16(2 * j, 2 * j2)) += b * Q[j] * Q[j2];
+            ACC(pk16(2 * j + 1, 2 * j2 + 1)) += b * Q[j] * Q[j2];
+          }
+        }
+      }
+    }
+  }
+  // add the block into R and the CSR values (this launch owns its nodes)
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {
+    const int j = i & 3, ki = k + (i >> 2);
+    double2* r = reinterpret_cast<double2*>(R) + int64_t(qr.v[j]) * (L + 1) + ki;
+    const double2 o = *r;
+    *r = make_double2(o.x + ACC(136 + 2 * i), o.y + ACC(136 + 2 * i + 1));
+  }
+  if (!NEED_J) return;
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {
+    const int j = i & 3, ki = k + (i >> 2);
+    const int m = (ki == 0 || ki == L) ? 2 : 3;
+    const int P = ki == 0 ? 0 : 3 * ki - 1;
+    const int kmin = ki == 0 ? 0 : ki - 1;
+#pragma unroll 1
+    for (int i2 = 0; i2 < 8; ++i2) {
+      const int j2 = i2 & 3, ki2 = k + (i2 >> 2);
+      const int slot = qr.slot[4 * j + j2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        double* row = vals + cs[j] + int64_t(4 * nc[j]) * P + int64_t(a) * 2 * nc[j] * m + slot * 2 * m +
+                      2 * (ki2 - kmin);
+        const int p = 2 * i + a;
+        const int q0 = 2 * i2, q1 = 2 * i2 + 1;
+        const double v0 = p <= q0 ? ACC(pk16(p, q0)) : ACC(pk16(q0, p));
+        const double v1 = p <= q1 ? ACC(pk16(p, q1)) : ACC(pk16(q1, p));
+        double2* rr = reinterpret_cast<double2*>(row);
+        const double2 o = *rr;
+        *rr = make_double2(o.x + v0, o.y + v1);
+      }
+    }
+  }
+#undef ACC
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+
+fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, int64_t n_quad,
+                          const int32_t* quad, int32_t L, const double* sigma, const double* thickness,
+                          const double* surface, const double* bed, const double* beta, const double* A_elem,
+                          int device, fo_mesh* out) {
+  auto bad = [](fo_status st, const std::string& msg) { set_error(msg); return st; };
+  if (!out || !p) return bad(FO_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (n_vert < 0 || n_quad < 0 || L < 1) return bad(FO_EINVAL, "bad sizes");
+  if (n_vert > 0 && (!xy || !quad || !thickness || !surface || !beta)) return bad(FO_EINVAL, "NULL array");
+  if (!(p->glen_n > 0.0) || !(p->A > 0.0) || p->eps_reg < 0.0) return bad(FO_EINVAL, "bad parameters");
+  if (sigma) {
+    if (sigma[0] != 0.0 || sigma[L] != 1.0) return bad(FO_EMESH, "sigma must run 0 .. 1");
+    for (int32_t k = 0; k < L; ++k)
+      if (!(sigma[k + 1] > sigma[k])) return bad(FO_EMESH, "sigma not strictly ascending");
+  }
+  std::vector<char> used(size_t(n_vert), 0);
+  for (int64_t t = 0; t < n_quad; ++t) {
+    const int32_t* v = quad + 4 * t;
+    for (int j = 0; j < 4; ++j)
+      if (v[j] < 0 || v[j] >= n_vert) return bad(FO_EMESH, "quad corner out of range");
+    for (int j = 0; j < 4; ++j) {   // convex and CCW: every corner turns left
+      const int32_t a = v[(j + 3) % 4], b = v[j], c = v[(j + 1) % 4];
+      const double cr = (xy[2 * b] - xy[2 * a]) * (xy[2 * c + 1] - xy[2 * b + 1]) -
+                        (xy[2 * b + 1] - xy[2 * a + 1]) * (xy[2 * c] - xy[2 * b]);
+      if (!(cr > 0.0)) return bad(FO_EMESH, "quad " + std::to_string(t) + " is not convex CCW");
+      used[size_t(b)] = 1;
+    }
+  }
+  for (int64_t c = 0; c < n_vert; ++c) {
+    if (!used[size_t(c)]) return bad(FO_EMESH, "vertex in no quad");
+    if (!(thickness[c] >= p->H_min)) return bad(FO_EMESH, "thickness below H_min");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return bad(FO_ECUDA, "no CUDA device available (libfo has no CPU path)");
+  }
+  if (device < 0 || device >= ndev) return bad(FO_EINVAL, "bad device ordinal");
+  fo_status st = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  if (st) return st;
+
+  fo_mesh m = new fo_mesh_s();
+  m->device = device;
+  m->p = *p;
+  m->L = L;
+  m->quad = true;
+  m->n_col = n_vert;
+  m->nA = n_vert;
+  m->n_tri = n_quad;
+  m->n_node = n_vert * (L + 1);
+  m->n_dof = 2 * m->n_node;
+  m->n_elem = n_quad * L;
+  m->n_owned_dof = m->n_dof;
+  m->glob.resize(size_t(n_vert));
+  for (int64_t c = 0; c < n_vert; ++c) m->glob[size_t(c)] = c;
+  m->tri_glob.resize(size_t(n_quad));
+  for (int64_t t = 0; t < n_quad; ++t) m->tri_glob[size_t(t)] = t;
+  // coupling lists: every corner of every quad around the column, sorted
+  std::vector<std::vector<int32_t>> lists(static_cast<size_t>(n_vert));
+  for (int64_t c = 0; c < n_vert; ++c) lists[size_t(c)].push_back(int32_t(c));
+  for (int64_t t = 0; t < n_quad; ++t)
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) lists[size_t(quad[4 * t + i])].push_back(quad[4 * t + j]);
+  m->nbr_ptr.assign(size_t(n_vert) + 1, 0);
+  for (int64_t c = 0; c < n_vert; ++c) {
+    auto& l = lists[size_t(c)];
+    std::sort(l.begin(), l.end());
+    l.erase(std::unique(l.begin(), l.end()), l.end());
+    if (l.size() > 255) { fo_mesh_destroy(m); return bad(FO_EMESH, "column couples to more than 254 neighbours"); }
+    m->nbr.insert(m->nbr.end(), l.begin(), l.end());
+    m->nbr_ptr[size_t(c) + 1] = int64_t(m->nbr.size());
+  }
+  m->colstart.assign(size_t(n_vert) + 1, 0);
+  for (int64_t c = 0; c < n_vert; ++c)
+    m->colstart[size_t(c) + 1] = m->colstart[size_t(c)] +
+                                 4 * (m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)]) * (3 * int64_t(L) + 1);
+  m->nnz = m->colstart.back();
+  m->sigma.resize(size_t(L) + 1);
+  for (int32_t k = 0; k <= L; ++k) m->sigma[size_t(k)] = sigma ? sigma[k] : double(k) / double(L);
+  m->sigma[size_t(L)] = 1.0;
+  m->colrec.assign(size_t(n_vert), ColRec{});
+  for (int64_t c = 0; c < n_vert; ++c) {
+    ColRec& r = m->colrec[size_t(c)];
+    r.x = xy[2 * c];
+    r.y = xy[2 * c + 1];
+    r.H = thickness[c];
+    r.base = surface[c] - thickness[c];
+    const bool floating = bed && (p->rho * thickness[c] < -p->rho_w * bed[c]);
+    r.beta = floating ? 0.0 : beta[c];
+    r.cs_n = (m->colstart[size_t(c)] << 8) | (m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)]);
+  }
+  std::vector<QuadRec> qrec(static_cast<size_t>(n_quad));
+  for (int64_t t = 0; t < n_quad; ++t) {
+    QuadRec& q = qrec[size_t(t)];
+    for (int i = 0; i < 4; ++i) q.v[i] = quad[4 * t + i];
+    for (int i = 0; i < 4; ++i) {
+      const int32_t* b = m->nbr.data() + m->nbr_ptr[size_t(q.v[i])];
+      const int32_t* e = m->nbr.data() + m->nbr_ptr[size_t(q.v[i]) + 1];
+      for (int j = 0; j < 4; ++j) q.slot[4 * i + j] = uint8_t(std::lower_bound(b, e, q.v[j]) - b);
+    }
+  }
+  // greedy colouring: quads sharing a corner get different colours
+  std::vector<std::vector<int32_t>> vq(static_cast<size_t>(n_vert));
+  for (int64_t t = 0; t < n_quad; ++t)
+    for (int i = 0; i < 4; ++i) vq[size_t(quad[4 * t + i])].push_back(int32_t(t));
+  std::vector<int32_t> color(size_t(n_quad), -1);
+  int ncol = 0;
+  for (int64_t t = 0; t < n_quad; ++t) {
+    uint64_t taken = 0;
+    for (int i = 0; i < 4; ++i)
+      for (int32_t o : vq[size_t(quad[4 * t + i])])
+        if (color[size_t(o)] >= 0 && color[size_t(o)] < 64) taken |= 1ull << color[size_t(o)];
+    int c = 0;
+    while (c < 64 && ((taken >> c) & 1)) ++c;
+    if (c == 64) { fo_mesh_destroy(m); return bad(FO_EMESH, "quad colouring needs more than 64 colours"); }
+    color[size_t(t)] = c;
+    ncol = std::max(ncol, c + 1);
+  }
+  m->hex_color_ptr.assign(size_t(ncol) + 1, 0);
+  for (int64_t t = 0; t < n_quad; ++t) m->hex_color_ptr[size_t(color[size_t(t)]) + 1]++;
+  for (int c = 0; c < ncol; ++c) m->hex_color_ptr[size_t(c) + 1] += m->hex_color_ptr[size_t(c)];
+  std::vector<int32_t> ids(static_cast<size_t>(n_quad));
+  {
+    std::vector<int64_t> pos(m->hex_color_ptr.begin(), m->hex_color_ptr.end() - 1);
+    for (int64_t t = 0; t < n_quad; ++t) ids[size_t(pos[size_t(color[size_t(t)])]++)] = int32_t(t);
+  }
+  auto up = [](void** dst, const void* src, size_t bytes) {
+    if (bytes == 0) return FO_OK;
+    fo_status s = cuda_status(cudaMalloc(dst, bytes), "cudaMalloc");
+    if (!s) s = cuda_status(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    return s;
+  };
+  st = up(reinterpret_cast<void**>(&m->d_col), m->colrec.data(), m->colrec.size() * sizeof(ColRec));
+  if (!st) st = up(reinterpret_cast<void**>(&m->d_sigma), m->sigma.data(), m->sigma.size() * sizeof(double));
+  if (!st) st = up(reinterpret_cast<void**>(&m->d_quad), qrec.data(), qrec.size() * sizeof(QuadRec));
+  if (!st) st = up(reinterpret_cast<void**>(&m->d_hex_ids), ids.data(), ids.size() * sizeof(int32_t));
+  if (!st && A_elem && m->n_elem > 0) {
+    std::vector<double> afac(static_cast<size_t>(m->n_elem));
+    for (int64_t i = 0; i < m->n_elem; ++i) {
+      if (!(A_elem[i] > 0.0)) { st = bad(FO_EINVAL, "A_elem must be > 0"); break; }
+      afac[size_t(i)] = std::pow(A_elem[i], -1.0 / p->glen_n);
+    }
+    if (!st) st = up(reinterpret_cast<void**>(&m->d_A), afac.data(), afac.size() * sizeof(double));
+    m->has_A_elem = true;
+  }
+  if (st) { fo_mesh_destroy(m); return st; }
+  *out = m;
+  return FO_OK;
+}
+
+fo_status launch_hex(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s) {
+  const bool need_j = d_vals != nullptr;
+  double* R = d_R;
+  if (!R) {
+    if (!m->d_scratch_R) {
+      fo_status st = cuda_status(cudaMalloc(&m->d_scratch_R, sizeof(double) * m->n_dof), "cudaMalloc");
+      if (st) return st;
+    }
+    R = m->d_scratch_R;
+  }
+  fo_status st = cuda_status(cudaMemsetAsync(R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
+  if (!st && need_j) st = cuda_status(cudaMemsetAsync(d_vals, 0, sizeof(double) * m->nnz, s), "cudaMemsetAsync");
+  if (st) return st;
+  const size_t smem = sizeof(double) * kHexAcc * kHexThreads;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hex_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(hex_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(hex_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(hex_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  const KParams kp = make_kparams(m);
+  const bool n3 = m->p.glen_n == 3.0;
+  int launches = 0;
+  const int ncol = int(m->hex_color_ptr.size()) - 1;
+  for (int kpar = 0; kpar < 2 && kpar < m->L; ++kpar)
+    for (int c = 0; c < ncol; ++c) {
+      const int n = int(m->hex_color_ptr[size_t(c) + 1] - m->hex_color_ptr[size_t(c)]);
+      const int nk = (m->L - kpar + 1) / 2;
+      const int64_t items = int64_t(n) * nk;
+      if (items == 0) continue;
+      const unsigned blocks = unsigned((items + kHexThreads - 1) / kHexThreads);
+      const int32_t* ids = m->d_hex_ids + m->hex_color_ptr[size_t(c)];
+      if (need_j) {
+        if (n3) hex_kernel<true, true><<<blocks, kHexThreads, smem, s>>>(m->d_col, m->d_quad, ids, n, kpar, m->d_sigma, m->d_A, kp, d_U, R, d_vals);
+        else hex_kernel<true, false><<<blocks, kHexThreads, smem, s>>>(m->d_col, m->d_quad, ids, n, kpar, m->d_sigma, m->d_A, kp, d_U, R, d_vals);
+      } else {
+        if (n3) hex_kernel<false, true><<<blocks, kHexThreads, smem, s>>>(m->d_col, m->d_quad, ids, n, kpar, m->d_sigma, m->d_A, kp, d_U, R, nullptr);
+        else hex_kernel<false, false><<<blocks, kHexThreads, smem, s>>>(m->d_col, m->d_quad, ids, n, kpar, m->d_sigma, m->d_A, kp, d_U, R, nullptr);
+      }
+      st = cuda_status(cudaGetLastError(), "hex_kernel launch");
+      if (st) return st;
+      ++launches;
+    }
+  m->last_launches = launches;
+  return FO_OK;
+}
+
+}  // namespace fo
+
+using namespace fo;
+
+extern "C" {
+
+fo_status fo_mesh_create_quad(const fo_params* p, int64_t n_vert, const double* xy, int64_t n_quad,
+                              const int32_t* quad, int32_t n_layers, const double* sigma,
+                              const double* thickness, const double* surface, const double* bed,
+                              const double* beta, const double* A_elem, int device, fo_mesh* out) {
+  return hex_create_impl(p, n_vert, xy, n_quad, quad, n_layers, sigma, thickness, surface, bed, beta, A_elem,
+                         device, out);
+}
+
+}  // extern "C"

@@ -574,6 +574,7 @@ fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, do
 
 fo_status fo_set_lateral(fo_mesh m, int enable) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (enable && m->quad) return fail(FO_EINVAL, "the lateral term is defined on wedge faces only");
   if (enable && m->elem_type != FO_ELEM_WEDGE)
     return fail(FO_EINVAL, "the lateral term is defined on wedge faces (FO_ELEM_WEDGE only)");
   m->lateral = enable != 0;
@@ -582,6 +583,7 @@ fo_status fo_set_lateral(fo_mesh m, int enable) {
 
 fo_status fo_set_element(fo_mesh m, fo_element type) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (m->quad) return fail(FO_EINVAL, "a quadrilateral mesh always uses hexahedra");
   if (type != FO_ELEM_WEDGE && type != FO_ELEM_TET3) return fail(FO_EINVAL, "unknown element type");
   if (type == FO_ELEM_TET3 && (m->lateral || m->scatter != FO_SCATTER_OWNER))
     return fail(FO_EINVAL, "FO_ELEM_TET3 needs the owner scatter and no lateral term");
@@ -623,6 +625,7 @@ fo_status fo_set_element(fo_mesh m, fo_element type) {
 
 fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (m->quad && s != FO_SCATTER_OWNER) return fail(FO_EINVAL, "hexahedra use the coloured scatter");
   if (s != FO_SCATTER_OWNER && m->elem_type != FO_ELEM_WEDGE)
     return fail(FO_EINVAL, "the atomic scatter supports FO_ELEM_WEDGE only");
   if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC) return fail(FO_EINVAL, "bad scatter");
@@ -672,6 +675,8 @@ void fo_mesh_destroy(fo_mesh m) {
   cudaFree(m->d_lat_cols);
   cudaFree(m->d_lat_faces);
   cudaFree(m->d_lat_refs);
+  cudaFree(m->d_quad);
+  cudaFree(m->d_hex_ids);
   cudaFree(m->d_nbr_ptr);
   cudaFree(m->d_nbr);
   cudaFree(m->d_self_slot);

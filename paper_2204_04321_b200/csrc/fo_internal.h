@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <vector_types.h>
+#include <cuda_runtime.h>
 #include <string>
 #include <vector>
 
@@ -26,6 +27,13 @@ struct alignas(8) TriRec {
   int32_t v[3];
   uint8_t slot[9];
   uint8_t pad[3];   // pad[0]: corners sorted by global vertex id, 2 bits each (NEXT-f4)
+};
+
+// NEXT-f4 hexahedra: per-quad record, 32 bytes: corner columns and the 16
+// slots slot[4 i + j] = position of corner j's column in corner i's list
+struct alignas(8) QuadRec {
+  int32_t v[4];
+  uint8_t slot[16];
 };
 
 // Triangles per patch of the owner-computes kernel (one thread per triangle
@@ -135,6 +143,10 @@ struct fo_mesh_s {
   double* d_T = nullptr;           // per-wedge T* (NEXT-f3) or nullptr
   double A0fac = 0.0, QnR = 0.0;   // Arrhenius constants folded for the kernels
   int elem_type = FO_ELEM_WEDGE;   // NEXT-f4 (fo_element_tet.cuh)
+  bool quad = false;               // NEXT-f4 hexahedral mesh (fo_hex.cu)
+  fo::QuadRec* d_quad = nullptr;
+  int32_t* d_hex_ids = nullptr;    // quads grouped by colour
+  std::vector<int64_t> hex_color_ptr;
   std::vector<int32_t> tri_ccw;    // the caller's (CCW) corner order, kept while
   std::vector<fo::TriRec> trirec_ccw;   // FO_ELEM_TET3 runs on global-id order
   // NEXT-f1 lateral margin term (fo_lateral.cu)
@@ -198,4 +210,6 @@ void free_patch_plan(fo_mesh m);
 // NEXT-f1 lateral margin term (fo_lateral.cu)
 fo_status build_lateral(fo_mesh m, int64_t n_tri_global, const int32_t* tri_global);
 fo_status launch_lateral(fo_mesh m, double* d_R, void* stream);
+// NEXT-f4 hexahedra (fo_hex.cu)
+fo_status launch_hex(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s);
 }  // namespace fo

@@ -87,6 +87,7 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
+  if (m->quad) return launch_hex(m, d_U, d_R, nullptr, s);
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
     st = launch_owner(m, d_U, d_R, nullptr, s);
   } else {
@@ -106,6 +107,7 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
+  if (m->quad) return launch_hex(m, d_U, d_R, d_vals, s);
   if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
     st = launch_owner(m, d_U, d_R, d_vals, s);
   } else {

@@ -47,6 +47,7 @@ _SIGS = {
     "fo_params_default": [P],
     "fo_mesh_create": [P, I64, P, I64, P, I32, P, P, P, P, P, P, C.c_int, P],
     "fo_mesh_create_part": [P, I64, P, I64, P, I32, P, P, P, P, P, P, P, I32, I32, C.c_int, P],
+    "fo_mesh_create_quad": [P, I64, P, I64, P, I32, P, P, P, P, P, P, C.c_int, P],
     "fo_partition": [I64, I32, P],
     "fo_mesh_info": [P, P, P, P, P],
     "fo_mesh_columns": [P, P, P, P, P, P],
@@ -307,7 +308,14 @@ class Mesh:
         a = cls._arrays(fp)
         h = C.c_void_p()
         n_vert, n_tri, L = a["xy"].shape[0], a["tri"].shape[0], a["sigma"].size - 1
-        if part is None:
+        if getattr(fp, "elem_type", 0) == 2:   # NEXT-f4: quadrilateral footprint, hexahedra
+            if part is not None:
+                raise FoError(FO_EINVAL, "fo_mesh_create_quad", "hexahedral meshes are single-domain")
+            st = lib().fo_mesh_create_quad(C.byref(p), n_vert, _ptr(a["xy"]), n_tri, _ptr(a["tri"]), L,
+                                           _ptr(a["sigma"]), _ptr(a["H"]), _ptr(a["s"]), _ptr(a["b"]),
+                                           _ptr(a["beta"]), _ptr(a["A"]), device, C.byref(h))
+            check(st, "fo_mesh_create_quad")
+        elif part is None:
             st = lib().fo_mesh_create(C.byref(p), n_vert, _ptr(a["xy"]), n_tri, _ptr(a["tri"]), L,
                                       _ptr(a["sigma"]), _ptr(a["H"]), _ptr(a["s"]), _ptr(a["b"]),
                                       _ptr(a["beta"]), _ptr(a["A"]), device, C.byref(h))

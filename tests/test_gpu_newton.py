@@ -119,3 +119,18 @@ def test_newton_solves_c1_and_the_oracle_agrees(torch_cuda, ora_mod):
     # the velocity is physical: downslope (+x) flow on the ISMIP-HOM A slab
     u = Uh.reshape(fp.n_vert, fp.n_layers + 1, 2)[:, :, 0]
     assert u.mean() > 0.0
+
+
+def test_newton_solves_c1_hexahedra(torch_cuda, ora_mod):
+    """The consumer is element-agnostic (SpMV and the line preconditioner see
+    only columns): Newton on the quadrilateral C1 with trilinear hexahedra."""
+    torch = torch_cuda
+    from paper_2204_04321_b200 import fo, newton
+    fp = mg.to_quads(mg.ismip_hom_a(), 20)
+    mesh = fo.Mesh.from_footprint(fp)
+    U = torch.tensor(fp.U, device="cuda")
+    s = newton.NewtonSolver(mesh, restart=30, max_krylov=600)
+    rep = s.solve(U, rtol=1e-9, max_newton=40, krylov_rtol=1e-6)
+    assert rep.converged, rep
+    R, M, _ = ora_mod.Oracle(fp).residual(U.cpu().numpy())
+    assert np.abs(R).max() <= 1e-8 * np.abs(M).max()

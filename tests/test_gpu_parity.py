@@ -27,7 +27,7 @@ def torch_cuda():
 def gpu_assemble(torch, fp, params=None, scatter=None, lateral=False):
     from paper_2204_04321_b200 import fo
     mesh = fo.Mesh.from_footprint(fp, params=params)
-    if getattr(fp, "elem_type", 0):
+    if getattr(fp, "elem_type", 0) == 1:
         mesh.set_element(fp.elem_type)
     if lateral:
         mesh.set_lateral(True)
@@ -162,6 +162,24 @@ def test_parity_tetrahedra(torch_cuda, ora_mod, case):
     fp.elem_type = 1
     g = gpu_assemble(torch_cuda, fp)
     check_parity(ora_mod.Oracle(fp), g, fp=fp)
+
+
+@pytest.mark.parametrize("case", ["C1-quads", "slab-quads-distorted", "quads-temperature"])
+def test_parity_hexahedra(torch_cuda, ora_mod, case):
+    """NEXT-f4: quadrilateral footprint, 8-node trilinear hexahedra (P:478,
+    reading L23), coloured deterministic scatter."""
+    if case == "C1-quads":
+        fp = mg.to_quads(mg.ismip_hom_a(nx=10, n_layers=5), 10)
+    elif case == "slab-quads-distorted":
+        fp = mg.to_quads(mg.slab(nx=7, n_layers=4, distort=0.2), 7)
+    else:
+        fp = mg.with_temperature(mg.to_quads(mg.ismip_hom_a(nx=6, n_layers=3), 6))
+    g = gpu_assemble(torch_cuda, fp)
+    check_parity(ora_mod.Oracle(fp), g, fp=fp)
+    import torch
+    R2, V2 = g["mesh"].jacobian(torch.tensor(fp.U, device="cuda"))
+    torch.cuda.synchronize()
+    assert np.array_equal(R2.cpu().numpy(), g["RJ"]) and np.array_equal(V2.cpu().numpy(), g["vals"])
 
 
 def test_tetrahedra_partitioned_and_rejections(torch_cuda, ora_mod):

@@ -58,3 +58,19 @@ mesh.set_lateral(False)
 mesh.set_element(1)
 line("f4_tet3", timeit(jac), "R + J, three P1 tetrahedra per prism (14.4 M tets)")
 line("f4_tet3_r_only", timeit(lambda: mesh.residual(U, R)), "R only, tetrahedra")
+
+# hexahedra on a quadrilateral footprint of C3 size (700 x 700 quads x 10 layers)
+fq = mg.to_quads(mg.ismip_hom_a(nx=700, n_layers=10), 700)
+mq = fo.Mesh.from_footprint(fq)
+gq = mq.graph()
+Uq = torch.tensor(fq.U, device="cuda")
+Rq = torch.empty(mq.n_dofs, dtype=torch.float64, device="cuda")
+Vq = torch.empty(gq.nnz, dtype=torch.float64, device="cuda")
+ms = timeit(lambda: mq.jacobian(Uq, gq, Rq, Vq))
+print(json.dumps({"variant": "f4_hex8", "workload": "700x700 quads x 10 layers", "wedges": fq.n_elem,
+                  "ms": round(ms, 4), "Melem_s": round(fq.n_elem / ms / 1e3, 1), "launches": mq.last_launch_count(),
+                  "note": "R + J, 8-node trilinear hexahedra, coloured scatter"}), flush=True)
+ms = timeit(lambda: mq.residual(Uq, Rq))
+print(json.dumps({"variant": "f4_hex8_r_only", "workload": "700x700 quads x 10 layers", "wedges": fq.n_elem,
+                  "ms": round(ms, 4), "Melem_s": round(fq.n_elem / ms / 1e3, 1), "launches": mq.last_launch_count(),
+                  "note": "R only, hexahedra"}), flush=True)
