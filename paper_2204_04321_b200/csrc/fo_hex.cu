@@ -145,7 +145,7 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
       ACC(136 + 2 * i + 1) += fma(c, g[2 * i + 1], bw * sy * N[i]);
     }
     if (NEED_J) {
-#pragma unroll 1
+#pragma unroll
       for (int i = 0; i < 8; ++i) {
 #pragma unroll
         for (int i2 = 0; i2 < 8; ++i2) {
