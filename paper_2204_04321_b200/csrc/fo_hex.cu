@@ -6,7 +6,8 @@
 // f_l(zeta) with the physical gradients from the generic 3x3 inverse of the
 // isoparametric map (the footprint map is bilinear, so nothing separates as for
 // the wedge), J = sum_q w_q [2 mu_q H_q - d_q g_q g_q^T] accumulated in the
-// thread's shared-memory block (136 upper-triangle values + 16 residual).
+// thread's registers in three passes (bottom-bottom with the residual, bottom-
+// top, top-top) that re-evaluate the point data.
 // Basal term: 2 x 2 Gauss on the bilinear bottom face, true 3D area element.
 //
 // Scatter: COLOURED.  Quads are greedily coloured so that no two quads of a
@@ -30,30 +31,127 @@ namespace fo {
 
 namespace {
 
-constexpr int kHexThreads = 64;
-constexpr int kHexAcc = 136 + 16;   // upper triangle of the 16 x 16 block + residual
+constexpr int kHexThreads = 128;
 
-__device__ __forceinline__ int pk16(int p, int q) {   // packed upper triangle, p <= q
-  return p * 16 - (p * (p - 1)) / 2 + (q - p);
+
+// Geometry and velocities of one hexahedron (registers)
+struct HexIn {
+  double X[4], Y[4], Zb[4], Zt[4], S[4], Uu[8], Uv[8], B[4];
+  double Afac;
+};
+
+// basis, physical gradients G and weight W = det J at Gauss point qp
+__device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8], double G[8][3]) {
+  constexpr double gz = 0.57735026918962576451;
+  const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
+  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+  double dN[8][3];
+  double J00 = 0, J01 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0, J20 = 0, J21 = 0, J22 = 0;
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = j + 4 * l;
+      const double fq = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+      const double fz = l == 0 ? 0.5 * (1.0 - zeta) : 0.5 * (1.0 + zeta);
+      N[i] = fq * fz;
+      dN[i][0] = 0.25 * cxi[j] * (1.0 + ceta[j] * eta) * fz;
+      dN[i][1] = 0.25 * ceta[j] * (1.0 + cxi[j] * xi) * fz;
+      dN[i][2] = fq * (l == 0 ? -0.5 : 0.5);
+      const double z = l == 0 ? h.Zb[j] : h.Zt[j];
+      J00 = fma(h.X[j], dN[i][0], J00); J01 = fma(h.X[j], dN[i][1], J01); J02 = fma(h.X[j], dN[i][2], J02);
+      J10 = fma(h.Y[j], dN[i][0], J10); J11 = fma(h.Y[j], dN[i][1], J11); J12 = fma(h.Y[j], dN[i][2], J12);
+      J20 = fma(z, dN[i][0], J20); J21 = fma(z, dN[i][1], J21); J22 = fma(z, dN[i][2], J22);
+    }
+  const double c00 = J11 * J22 - J12 * J21, c01 = J12 * J20 - J10 * J22, c02 = J10 * J21 - J11 * J20;
+  const double det = J00 * c00 + J01 * c01 + J02 * c02;
+  const double id = 1.0 / det;
+  const double i00 = c00 * id, i01 = (J02 * J21 - J01 * J22) * id, i02 = (J01 * J12 - J02 * J11) * id;
+  const double i10 = c01 * id, i11 = (J00 * J22 - J02 * J20) * id, i12 = (J02 * J10 - J00 * J12) * id;
+  const double i20 = c02 * id, i21 = (J01 * J20 - J00 * J21) * id, i22 = (J00 * J11 - J01 * J10) * id;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    G[i][0] = i00 * dN[i][0] + i10 * dN[i][1] + i20 * dN[i][2];
+    G[i][1] = i01 * dN[i][0] + i11 * dN[i][1] + i21 * dN[i][2];
+    G[i][2] = i02 * dN[i][0] + i12 * dN[i][1] + i22 * dN[i][2];
+  }
+  return det;   // Gauss weights 1
 }
 
+// viscosity factors and the strain-rate gradients g_{a,i} = eps_a . grad phi_i
+template <bool N3>
+__device__ __forceinline__ void hex_visc(const HexIn& h, const double G[8][3], double W, const KParams& kp,
+                                         double g[16], double& c, double& d) {
+  double ux = 0, uy = 0, uz = 0, vx = 0, vy = 0, vz = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ux = fma(h.Uu[i], G[i][0], ux); uy = fma(h.Uu[i], G[i][1], uy); uz = fma(h.Uu[i], G[i][2], uz);
+    vx = fma(h.Uv[i], G[i][0], vx); vy = fma(h.Uv[i], G[i][1], vy); vz = fma(h.Uv[i], G[i][2], vz);
+  }
+  const double exy = 0.5 * (uy + vx), exz = 0.5 * uz, eyz = 0.5 * vz;
+  const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
+  const double qe = qq + kp.eps;
+  if (N3) {
+    const double y = rcbrt(qe);
+    c = W * h.Afac * y;
+    d = c * (y * y * y) * (1.0 / 3.0);
+  } else {
+    c = W * h.Afac * pow(qe, (1.0 - kp.glen_n) / (2.0 * kp.glen_n));
+    d = c * ((kp.glen_n - 1.0) / (2.0 * kp.glen_n)) / qe;
+  }
+  const double e1x = 2.0 * ux + vy, e2y = ux + 2.0 * vy;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    g[2 * i] = fma(e1x, G[i][0], fma(exy, G[i][1], exz * G[i][2]));
+    g[2 * i + 1] = fma(exy, G[i][0], fma(e2y, G[i][1], eyz * G[i][2]));
+  }
+}
+
+// J entry (row dof p, column dof p2) at one point: c H - d g g^T
+__device__ __forceinline__ double hex_jentry(const double G[8][3], const double g[16], double c, double d, int p,
+                                             int p2) {
+  const int i = p >> 1, a = p & 1, i2 = p2 >> 1, b = p2 & 1;
+  const double xx = G[i][0] * G[i2][0], yy = G[i][1] * G[i2][1], zz = G[i][2] * G[i2][2];
+  const double xy = G[i][0] * G[i2][1], yx = G[i][1] * G[i2][0];
+  double hh;
+  if (a == 0 && b == 0) hh = fma(2.0, xx, 0.5 * (yy + zz));
+  else if (a == 1 && b == 1) hh = fma(2.0, yy, 0.5 * (xx + zz));
+  else if (a == 0) hh = fma(0.5, yx, xy);
+  else hh = fma(0.5, xy, yx);
+  return fma(c, hh, -d * g[p] * g[p2]);
+}
+
+// add v0, v1 (column comps 0, 1) to row (node i, comp a) at column node i2
+__device__ __forceinline__ void hex_add(double* __restrict__ vals, const QuadRec& qr, const int64_t cs[4],
+                                        const int nc[4], int L, int k, int i, int a, int i2, double v0, double v1) {
+  const int j = i & 3, ki = k + (i >> 2), j2 = i2 & 3, ki2 = k + (i2 >> 2);
+  const int m = (ki == 0 || ki == L) ? 2 : 3;
+  const int P = ki == 0 ? 0 : 3 * ki - 1;
+  const int kmin = ki == 0 ? 0 : ki - 1;
+  double2* rr = reinterpret_cast<double2*>(vals + cs[j] + int64_t(4 * nc[j]) * P + int64_t(a) * 2 * nc[j] * m +
+                                           int(qr.slot[4 * j + j2]) * 2 * m + 2 * (ki2 - kmin));
+  const double2 o = *rr;
+  *rr = make_double2(o.x + v0, o.y + v1);
+}
+
+// One thread per hexahedron; the 16 x 16 block is accumulated in registers in
+// three passes over the 8 points -- (bottom, bottom) with the residual and the
+// basal term, (bottom, top), (top, top) -- re-evaluating the point data in
+// each pass rather than keeping 136 accumulators live; after each pass the
+// block is added into the CSR values (both orientations, J symmetric).
 template <bool NEED_J, bool N3>
 __global__ void __launch_bounds__(kHexThreads)
 hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, const int32_t* __restrict__ ids,
            int n_ids, int kpar, const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
            const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
-  extern __shared__ double hsm[];
   const int L = kp.L;
   const int nk = (L - kpar + 1) / 2;   // layers k = kpar, kpar + 2, ...
   const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= int64_t(n_ids) * nk) return;
   const int qi = __ldg(ids + item / nk);
   const int k = kpar + 2 * int(item % nk);
-  double* acc = hsm + threadIdx.x;   // acc[i * kHexThreads]
-#define ACC(i) acc[(i) * kHexThreads]
-  for (int i = 0; i < kHexAcc; ++i) ACC(i) = 0.0;
   const QuadRec qr = quads[qi];
-  double X[8], Y[8], Z[8], S[8], Uu[8], Uv[8], B[4];
+  HexIn h;
   int64_t cs[4];
   int nc[4];
   const double s0 = __ldg(sigma + k), s1 = __ldg(sigma + k + 1);
@@ -62,109 +160,50 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
     const ColRec c = col[qr.v[j]];
     cs[j] = c.cs_n >> 8;
     nc[j] = int(c.cs_n & 255);
-    X[j] = X[j + 4] = c.x;
-    Y[j] = Y[j + 4] = c.y;
-    Z[j] = fma(s0, c.H, c.base);
-    Z[j + 4] = fma(s1, c.H, c.base);
-    S[j] = S[j + 4] = c.base + c.H;
-    B[j] = c.beta;
+    h.X[j] = c.x;
+    h.Y[j] = c.y;
+    h.Zb[j] = fma(s0, c.H, c.base);
+    h.Zt[j] = fma(s1, c.H, c.base);
+    h.S[j] = c.base + c.H;
+    h.B[j] = c.beta;
     const int64_t node = int64_t(qr.v[j]) * (L + 1) + k;
     const double2 ub = __ldg(reinterpret_cast<const double2*>(U) + node);
     const double2 ut = __ldg(reinterpret_cast<const double2*>(U) + node + 1);
-    Uu[j] = ub.x; Uv[j] = ub.y; Uu[j + 4] = ut.x; Uv[j + 4] = ut.y;
+    h.Uu[j] = ub.x; h.Uv[j] = ub.y; h.Uu[j + 4] = ut.x; h.Uv[j + 4] = ut.y;
   }
-  const double Afac = wedge_afac(kp, Aw, qi, k);
-  const double ex1 = (1.0 - kp.glen_n) / (2.0 * kp.glen_n), kap = (kp.glen_n - 1.0) / (2.0 * kp.glen_n);
-  constexpr double gz = 0.57735026918962576451;
-  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+  h.Afac = wedge_afac(kp, Aw, qi, k);
+  // ---- pass 1: residual, (bottom, bottom) block, basal term
+  double r[16], bb[36];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 36; ++i) bb[i] = 0.0;
 #pragma unroll 1
   for (int qp = 0; qp < 8; ++qp) {
-    const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
-    double N[8], dN[8][3];
+    double N[8], G[8][3], g[16], c, d;
+    const double W = hex_point(h, qp, N, G);
+    hex_visc<N3>(h, G, W, kp, g, c, d);
+    double sx = 0, sy = 0;
 #pragma unroll
-    for (int l = 0; l < 2; ++l)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = j + 4 * l;
-        const double fq = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
-        const double fz = l == 0 ? 0.5 * (1.0 - zeta) : 0.5 * (1.0 + zeta);
-        N[i] = fq * fz;
-        dN[i][0] = 0.25 * cxi[j] * (1.0 + ceta[j] * eta) * fz;
-        dN[i][1] = 0.25 * ceta[j] * (1.0 + cxi[j] * xi) * fz;
-        dN[i][2] = fq * (l == 0 ? -0.5 : 0.5);
-      }
-    double J00 = 0, J01 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0, J20 = 0, J21 = 0, J22 = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      J00 = fma(X[i], dN[i][0], J00); J01 = fma(X[i], dN[i][1], J01); J02 = fma(X[i], dN[i][2], J02);
-      J10 = fma(Y[i], dN[i][0], J10); J11 = fma(Y[i], dN[i][1], J11); J12 = fma(Y[i], dN[i][2], J12);
-      J20 = fma(Z[i], dN[i][0], J20); J21 = fma(Z[i], dN[i][1], J21); J22 = fma(Z[i], dN[i][2], J22);
-    }
-    const double c00 = J11 * J22 - J12 * J21, c01 = J12 * J20 - J10 * J22, c02 = J10 * J21 - J11 * J20;
-    const double det = J00 * c00 + J01 * c01 + J02 * c02;
-    const double id = 1.0 / det;
-    // inverse (row r = d(xi_r)/d(x)): inv[c][r] in the oracle's notation
-    const double i00 = c00 * id, i01 = (J02 * J21 - J01 * J22) * id, i02 = (J01 * J12 - J02 * J11) * id;
-    const double i10 = c01 * id, i11 = (J00 * J22 - J02 * J20) * id, i12 = (J02 * J10 - J00 * J12) * id;
-    const double i20 = c02 * id, i21 = (J01 * J20 - J00 * J21) * id, i22 = (J00 * J11 - J01 * J10) * id;
-    double G[8][3];
-    double ux = 0, uy = 0, uz = 0, vx = 0, vy = 0, vz = 0, sx = 0, sy = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      G[i][0] = i00 * dN[i][0] + i10 * dN[i][1] + i20 * dN[i][2];
-      G[i][1] = i01 * dN[i][0] + i11 * dN[i][1] + i21 * dN[i][2];
-      G[i][2] = i02 * dN[i][0] + i12 * dN[i][1] + i22 * dN[i][2];
-      ux = fma(Uu[i], G[i][0], ux); uy = fma(Uu[i], G[i][1], uy); uz = fma(Uu[i], G[i][2], uz);
-      vx = fma(Uv[i], G[i][0], vx); vy = fma(Uv[i], G[i][1], vy); vz = fma(Uv[i], G[i][2], vz);
-      sx = fma(S[i], G[i][0], sx); sy = fma(S[i], G[i][1], sy);
-    }
-    const double W = det;   // Gauss weights 1
-    const double exy = 0.5 * (uy + vx), exz = 0.5 * uz, eyz = 0.5 * vz;
-    const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
-    const double qe = qq + kp.eps;
-    double c, d;
-    if (N3) {
-      const double y = rcbrt(qe);
-      c = W * Afac * y;
-      d = c * (y * y * y) * (1.0 / 3.0);
-    } else {
-      c = W * Afac * pow(qe, ex1);
-      d = c * kap / qe;
-    }
-    const double e1x = 2.0 * ux + vy, e2y = ux + 2.0 * vy;
-    double g[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      g[2 * i] = fma(e1x, G[i][0], fma(exy, G[i][1], exz * G[i][2]));
-      g[2 * i + 1] = fma(exy, G[i][0], fma(e2y, G[i][1], eyz * G[i][2]));
-    }
+    for (int i = 0; i < 8; ++i) { sx = fma(h.S[i & 3], G[i][0], sx); sy = fma(h.S[i & 3], G[i][1], sy); }
     const double bw = W * kp.rg;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      ACC(136 + 2 * i) += fma(c, g[2 * i], bw * sx * N[i]);
-      ACC(136 + 2 * i + 1) += fma(c, g[2 * i + 1], bw * sy * N[i]);
+      r[2 * i] += fma(c, g[2 * i], bw * sx * N[i]);
+      r[2 * i + 1] += fma(c, g[2 * i + 1], bw * sy * N[i]);
     }
     if (NEED_J) {
+      int e = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int p = 0; p < 8; ++p)
 #pragma unroll
-        for (int i2 = 0; i2 < 8; ++i2) {
-          if (i2 < i) continue;
-          const double xx = G[i][0] * G[i2][0], yy = G[i][1] * G[i2][1], zz = G[i][2] * G[i2][2];
-          const double xy = G[i][0] * G[i2][1], yx = G[i][1] * G[i2][0];
-          const double huu = fma(2.0, xx, 0.5 * (yy + zz)), hvv = fma(2.0, yy, 0.5 * (xx + zz));
-          const double huv = fma(0.5, yx, xy), hvu = fma(0.5, xy, yx);
-          const int p = 2 * i, p2 = 2 * i2;
-          ACC(pk16(p, p2)) += fma(c, huu, -d * g[p] * g[p2]);
-          ACC(pk16(p, p2 + 1)) += fma(c, huv, -d * g[p] * g[p2 + 1]);
-          if (i2 > i) ACC(pk16(p + 1, p2)) += fma(c, hvu, -d * g[p + 1] * g[p2]);
-          ACC(pk16(p + 1, p2 + 1)) += fma(c, hvv, -d * g[p + 1] * g[p2 + 1]);
-        }
-      }
+        for (int p2 = p; p2 < 8; ++p2) bb[e++] += hex_jentry(G, g, c, d, p, p2);
     }
   }
   if (k == 0) {   // basal Robin term on the bilinear bottom face
-#pragma unroll 1
+    constexpr double gz = 0.57735026918962576451;
+    const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+#pragma unroll
     for (int qp = 0; qp < 4; ++qp) {
       const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz;
       double Q[4], tx0 = 0, tx1 = 0, tx2 = 0, ty0 = 0, ty1 = 0, ty2 = 0;
@@ -172,62 +211,113 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
       for (int j = 0; j < 4; ++j) {
         Q[j] = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
         const double dxi = 0.25 * cxi[j] * (1.0 + ceta[j] * eta), deta = 0.25 * ceta[j] * (1.0 + cxi[j] * xi);
-        tx0 = fma(dxi, X[j], tx0); tx1 = fma(dxi, Y[j], tx1); tx2 = fma(dxi, Z[j], tx2);
-        ty0 = fma(deta, X[j], ty0); ty1 = fma(deta, Y[j], ty1); ty2 = fma(deta, Z[j], ty2);
+        tx0 = fma(dxi, h.X[j], tx0); tx1 = fma(dxi, h.Y[j], tx1); tx2 = fma(dxi, h.Zb[j], tx2);
+        ty0 = fma(deta, h.X[j], ty0); ty1 = fma(deta, h.Y[j], ty1); ty2 = fma(deta, h.Zb[j], ty2);
       }
       const double cx = tx1 * ty2 - tx2 * ty1, cy = tx2 * ty0 - tx0 * ty2, cz = tx0 * ty1 - tx1 * ty0;
       const double w = sqrt(cx * cx + cy * cy + cz * cz);
-      const double b = w * (Q[0] * B[0] + Q[1] * B[1] + Q[2] * B[2] + Q[3] * B[3]);
-      const double u = Q[0] * Uu[0] + Q[1] * Uu[1] + Q[2] * Uu[2] + Q[3] * Uu[3];
-      const double v = Q[0] * Uv[0] + Q[1] * Uv[1] + Q[2] * Uv[2] + Q[3] * Uv[3];
+      const double bq = w * (Q[0] * h.B[0] + Q[1] * h.B[1] + Q[2] * h.B[2] + Q[3] * h.B[3]);
+      const double u = Q[0] * h.Uu[0] + Q[1] * h.Uu[1] + Q[2] * h.Uu[2] + Q[3] * h.Uu[3];
+      const double v = Q[0] * h.Uv[0] + Q[1] * h.Uv[1] + Q[2] * h.Uv[2] + Q[3] * h.Uv[3];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        ACC(136 + 2 * j) += b * Q[j] * u;
-        ACC(136 + 2 * j + 1) += b * Q[j] * v;
-        if (NEED_J) {
+        r[2 * j] += bq * Q[j] * u;
+        r[2 * j + 1] += bq * Q[j] * v;
+      }
+      if (NEED_J) {
+        int e = 0;
 #pragma unroll
-          for (int j2 = j; j2 < 4; ++j2) {
-            ACC(pk16(2 * j, 2 * j2)) += b * Q[j] * Q[j2];
-            ACC(pk16(2 * j + 1, 2 * j2 + 1)) += b * Q[j] * Q[j2];
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int p2 = p; p2 < 8; ++p2) {
+            if ((p & 1) == (p2 & 1)) bb[e] += bq * Q[p >> 1] * Q[p2 >> 1];
+            ++e;
           }
-        }
       }
     }
   }
-  // add the block into R and the CSR values (this launch owns its nodes)
-#pragma unroll 1
+#pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int j = i & 3, ki = k + (i >> 2);
-    double2* r = reinterpret_cast<double2*>(R) + int64_t(qr.v[j]) * (L + 1) + ki;
-    const double2 o = *r;
-    *r = make_double2(o.x + ACC(136 + 2 * i), o.y + ACC(136 + 2 * i + 1));
+    double2* rr = reinterpret_cast<double2*>(R) + int64_t(qr.v[i & 3]) * (L + 1) + k + (i >> 2);
+    const double2 o = *rr;
+    *rr = make_double2(o.x + r[2 * i], o.y + r[2 * i + 1]);
   }
   if (!NEED_J) return;
-#pragma unroll 1
-  for (int i = 0; i < 8; ++i) {
-    const int j = i & 3, ki = k + (i >> 2);
-    const int m = (ki == 0 || ki == L) ? 2 : 3;
-    const int P = ki == 0 ? 0 : 3 * ki - 1;
-    const int kmin = ki == 0 ? 0 : ki - 1;
-#pragma unroll 1
-    for (int i2 = 0; i2 < 8; ++i2) {
-      const int j2 = i2 & 3, ki2 = k + (i2 >> 2);
-      const int slot = qr.slot[4 * j + j2];
+  // (bottom, bottom): rows of bottom node i, columns of bottom node i2
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int i2 = 0; i2 < 4; ++i2)
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
-        double* row = vals + cs[j] + int64_t(4 * nc[j]) * P + int64_t(a) * 2 * nc[j] * m + slot * 2 * m +
-                      2 * (ki2 - kmin);
-        const int p = 2 * i + a;
-        const int q0 = 2 * i2, q1 = 2 * i2 + 1;
-        const double v0 = p <= q0 ? ACC(pk16(p, q0)) : ACC(pk16(q0, p));
-        const double v1 = p <= q1 ? ACC(pk16(p, q1)) : ACC(pk16(q1, p));
-        double2* rr = reinterpret_cast<double2*>(row);
-        const double2 o = *rr;
-        *rr = make_double2(o.x + v0, o.y + v1);
+        double v[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int p = 2 * i + a, p2 = 2 * i2 + b;
+          const int lo = p < p2 ? p : p2, hi = p < p2 ? p2 : p;
+          v[b] = bb[lo * 8 - (lo * (lo - 1)) / 2 + (hi - lo)];
+        }
+        hex_add(vals, qr, cs, nc, L, k, i, a, i2, v[0], v[1]);
       }
+  // ---- pass 2: (bottom, top) block; written for both orientations
+  {
+    double bt[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) bt[i] = 0.0;
+#pragma unroll 1
+    for (int qp = 0; qp < 8; ++qp) {
+      double N[8], G[8][3], g[16], c, d;
+      const double W = hex_point(h, qp, N, G);
+      hex_visc<N3>(h, G, W, kp, g, c, d);
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int p2 = 0; p2 < 8; ++p2) bt[8 * p + p2] += hex_jentry(G, g, c, d, p, 8 + p2);
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          // row bottom node i, column top node 4 + i2
+          hex_add(vals, qr, cs, nc, L, k, i, a, 4 + i2, bt[8 * (2 * i + a) + 2 * i2], bt[8 * (2 * i + a) + 2 * i2 + 1]);
+          // row top node 4 + i2, column bottom node i (transpose)
+          hex_add(vals, qr, cs, nc, L, k, 4 + i2, a, i, bt[8 * (2 * i) + 2 * i2 + a], bt[8 * (2 * i + 1) + 2 * i2 + a]);
+        }
   }
-#undef ACC
+  // ---- pass 3: (top, top) block
+  {
+    double tt[36];
+#pragma unroll
+    for (int i = 0; i < 36; ++i) tt[i] = 0.0;
+#pragma unroll 1
+    for (int qp = 0; qp < 8; ++qp) {
+      double N[8], G[8][3], g[16], c, d;
+      const double W = hex_point(h, qp, N, G);
+      hex_visc<N3>(h, G, W, kp, g, c, d);
+      int e = 0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int p2 = p; p2 < 8; ++p2) tt[e++] += hex_jentry(G, g, c, d, 8 + p, 8 + p2);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          double v[2];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int p = 2 * i + a, p2 = 2 * i2 + b;
+            const int lo = p < p2 ? p : p2, hi = p < p2 ? p2 : p;
+            v[b] = tt[lo * 8 - (lo * (lo - 1)) / 2 + (hi - lo)];
+          }
+          hex_add(vals, qr, cs, nc, L, k, 4 + i, a, 4 + i2, v[0], v[1]);
+        }
+  }
 }
 
 }  // namespace
@@ -397,15 +487,7 @@ fo_status launch_hex(fo_mesh m, const double* d_U, double* d_R, double* d_vals, 
   fo_status st = cuda_status(cudaMemsetAsync(R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
   if (!st && need_j) st = cuda_status(cudaMemsetAsync(d_vals, 0, sizeof(double) * m->nnz, s), "cudaMemsetAsync");
   if (st) return st;
-  const size_t smem = sizeof(double) * kHexAcc * kHexThreads;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(hex_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(hex_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(hex_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(hex_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  const size_t smem = 0;
   const KParams kp = make_kparams(m);
   const bool n3 = m->p.glen_n == 3.0;
   int launches = 0;
