@@ -295,7 +295,7 @@ def test_symmetry_and_overwrite(torch_cuda):
     rp, col = g.to_host()
     import scipy.sparse as sp
     J = sp.csr_matrix((vals2.cpu().numpy(), col, rp), shape=(mesh.n_dofs, mesh.n_dofs))
-    assert abs(J - J.T).max() <= 1e-13 * abs(J).max()
+    assert abs(J - J.T).max() <= 1e-14 * abs(J).max()
 
 
 def test_host_buffer_entry_point(torch_cuda):
