@@ -163,6 +163,18 @@ FO_API fo_status fo_graph_to_host(fo_graph g, int64_t* row_ptr, int32_t* col_idx
 FO_API fo_status fo_graph_host(int64_t n_vert, int64_t n_tri, const int32_t* tri, int32_t n_layers,
                         int64_t* row_ptr, int32_t* col_idx, int64_t* nnz);
 
+/* Host-only check of the owner-computes scatter plan (no device; tests):
+ * builds the (part) mesh's patch plan as fo_mesh_create would and verifies
+ * that every coupling-list slot and residual of a column with rows is written
+ * by exactly one store (interior pair / multi-column fix-up) or by RED partial
+ * sums onto a zero-filled column, and that every element entry is gathered
+ * exactly once.  stats[8] = {patches, pairs, contributions, zero-filled
+ * columns, multi columns, slot violations, element violations, largest plan
+ * bytes}.  part_of_tri NULL: single domain.  Synchronous. */
+FO_API fo_status fo_plan_check_host(int64_t n_vert, const double* xy, int64_t n_tri, const int32_t* tri,
+                                    int32_t n_layers, const int32_t* part_of_tri, int32_t my_part,
+                                    int32_t n_parts, int64_t* stats);
+
 /* R = F(U): overwrites d_R[n_dofs].  d_U[n_dofs] fp64. */
 FO_API fo_status fo_assemble_residual(fo_mesh m, const double* d_U, double* d_R, void* stream);
 

@@ -274,7 +274,8 @@ fo_status mesh_create_impl(const fo_params* p, int64_t n_vert, const double* xy,
                            const int32_t* tri, int32_t L, const double* sigma,
                            const double* thickness, const double* surface, const double* bed,
                            const double* beta, const double* A_elem, const int32_t* part,
-                           int32_t my_part, int32_t n_parts, int device, fo_mesh* out) {
+                           int32_t my_part, int32_t n_parts, int device, fo_mesh* out,
+                           bool host_only = false) {
   if (!out) return fail(FO_EINVAL, "out is NULL");
   *out = nullptr;
   fo_status st = validate(p, n_vert, xy, n_tri, tri, L, sigma, thickness, surface, beta);
@@ -285,6 +286,7 @@ fo_status mesh_create_impl(const fo_params* p, int64_t n_vert, const double* xy,
       if (part[t] < 0 || part[t] >= n_parts) return fail(FO_EINVAL, "part_of_tri out of range");
   }
   int ndev = 0;
+  if (host_only) goto host_topology;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
     return fail(FO_ECUDA, "no CUDA device available (libfo has no CPU path)");
@@ -292,7 +294,7 @@ fo_status mesh_create_impl(const fo_params* p, int64_t n_vert, const double* xy,
   if (device < 0 || device >= ndev) return fail(FO_EINVAL, "bad device ordinal");
   st = cuda_status(cudaSetDevice(device), "cudaSetDevice");
   if (st) return st;
-
+host_topology:
   Topo T;
   st = build_topology(n_vert, n_tri, tri, L, part, my_part, T);
   if (st) return st;
@@ -340,6 +342,12 @@ fo_status mesh_create_impl(const fo_params* p, int64_t n_vert, const double* xy,
   m->colstart = std::move(T.colstart);
   m->trirec = std::move(T.trirec);
 
+  if (host_only) {   // the patch plan only, nothing on a device (fo_plan_check_host)
+    st = build_patch_plan(m, false);
+    if (st) { delete m; return st; }
+    *out = m;
+    return FO_OK;
+  }
   st = upload(&m->d_col, m->colrec.data(), m->colrec.size());
   if (!st) st = upload(&m->d_tri, m->trirec.data(), m->trirec.size());
   if (!st) st = upload(&m->d_sigma, m->sigma.data(), m->sigma.size());
@@ -369,6 +377,21 @@ using namespace fo;
 extern "C" {
 
 const char* fo_last_error(void) { return g_err.c_str(); }
+
+fo_status fo_plan_check_host(int64_t n_vert, const double* xy, int64_t n_tri, const int32_t* tri, int32_t n_layers,
+                             const int32_t* part_of_tri, int32_t my_part, int32_t n_parts, int64_t* stats) {
+  if (!stats) return fail(FO_EINVAL, "stats is NULL");
+  fo_params p;
+  fo_params_default(&p);
+  std::vector<double> H(size_t(n_vert), 1000.0), s(size_t(n_vert), 1000.0), beta(size_t(n_vert), 1.0);
+  fo_mesh m = nullptr;
+  fo_status st = mesh_create_impl(&p, n_vert, xy, n_tri, tri, n_layers, nullptr, H.data(), s.data(), nullptr,
+                                  beta.data(), nullptr, part_of_tri, my_part, n_parts, 0, &m, true);
+  if (st) return st;
+  st = plan_check(m, stats);
+  delete m;
+  return st;
+}
 
 fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, double Q) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");

@@ -205,8 +205,9 @@ fo_status cuda_status(int err, const char* what);   // err: cudaError_t
 fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* stream);
 fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_vals,
                           void* stream);
-fo_status build_patch_plan(fo_mesh m);
+fo_status build_patch_plan(fo_mesh m, bool upload = true);
 void free_patch_plan(fo_mesh m);
+fo_status plan_check(const fo_mesh m, int64_t* stats);
 // NEXT-f1 lateral margin term (fo_lateral.cu)
 fo_status build_lateral(fo_mesh m, int64_t n_tri_global, const int32_t* tri_global);
 fo_status launch_lateral(fo_mesh m, double* d_R, void* stream);

@@ -144,7 +144,7 @@ void free_patch_plan(fo_mesh m) {
   m->plan = PatchPlan();
 }
 
-fo_status build_patch_plan(fo_mesh m) {
+fo_status build_patch_plan(fo_mesh m, bool upload) {
   PatchPlan& P = m->plan;
   P = PatchPlan();
   const int64_t nt = m->n_tri;
@@ -241,6 +241,7 @@ fo_status build_patch_plan(fo_mesh m) {
     blob.resize((blob.size() + 15) / 16 * 16, 0);
     blob_off.push_back(int64_t(blob.size()));
   }
+  if (!upload) return FO_OK;
   fo_status st = upload_vec(&m->d_plan.t_begin, P.t_begin);
   if (!st) st = upload_vec(&m->d_plan.col_ptr, P.col_ptr);
   if (!st) st = upload_vec(&m->d_plan.pair_ptr, P.pair_ptr);
@@ -254,6 +255,92 @@ fo_status build_patch_plan(fo_mesh m) {
                                 sizeof(double) * kPartialStride * size_t(m->L + 1) * size_t(P.n_partials)),
                      "cudaMalloc");
   return st;
+}
+
+// Host check of a plan's coverage (fo_plan_check_host): every coupling-list
+// slot and residual of a column with rows must be written either by one
+// store (an interior column's pair; the fix-up of a multi column's self slot)
+// or by RED partial sums onto a zero-filled boundary column -- never both,
+// never neither; every element entry (t, j, j2) must be gathered exactly once,
+// by the pair of column v_j, slot of v_j2.  stats[8] = {patches, pairs,
+// contributions (pads excluded), zero-filled columns, multi columns,
+// slot / residual violations, element-entry violations, largest plan bytes}.
+fo_status plan_check(const fo_mesh m, int64_t* stats) {
+  const PatchPlan& P = m->plan;
+  const int64_t nk = m->nA + m->nB;
+  std::vector<int32_t> store(m->nbr.size(), 0), red(m->nbr.size(), 0);
+  std::vector<int32_t> rstore(size_t(m->n_col), 0), rred(size_t(m->n_col), 0);
+  std::vector<char> zeroed(size_t(m->n_col), 0), multi(size_t(m->n_col), 0);
+  for (int32_t c : P.zero_cols) zeroed[size_t(c)] = 1;
+  for (const MultiRec& r : P.multi) multi[size_t(r.c)] = 1;
+  std::vector<int32_t> seen(size_t(9 * m->n_tri), 0);
+  int64_t n_contrib = 0, bad_elem = 0;
+  for (int32_t p = 0; p < P.n_patches; ++p) {
+    const PlanCol* cols = P.cols.data() + P.col_ptr[size_t(p)];
+    const int32_t t0 = P.t_begin[size_t(p)];
+    for (int32_t q = P.pair_ptr[size_t(p)]; q < P.pair_ptr[size_t(p) + 1]; ++q) {
+      const PlanPair& pp = P.pairs[size_t(q)];
+      const PlanCol& pc = cols[pp.col];
+      const int64_t e = m->nbr_ptr[size_t(pc.c)] + pp.slot;
+      const bool interior = (pc.info >> 8) & 1;
+      const bool mself = ((pc.info >> 30) & 1) && pp.slot == ((pc.info >> 9) & 255);
+      if (mself) {
+        // written by the fix-up: counted once per column below
+      } else if (interior) {
+        store[size_t(e)]++;
+      } else {
+        red[size_t(e)]++;
+      }
+      for (int i = 0; i < pp.cnt; ++i) {
+        const uint32_t cb = P.contrib[size_t(P.contrib_ptr[size_t(p)] + pp.off + i)];
+        const int tl = int(cb & 255);
+        if (tl == kPatchTris) continue;   // pad
+        ++n_contrib;
+        const int j = int((cb >> 25) & 3);
+        const int o = int((cb >> 15) & 31);   // 12 j + 2 j2
+        const int j2 = (o - 12 * j) / 2;
+        const int64_t t = t0 + tl;
+        const TriRec& tr = m->trirec[size_t(t)];
+        if (tr.v[j] != pc.c || tr.slot[3 * j + j2] != pp.slot) ++bad_elem;
+        seen[size_t(9 * t + 3 * j + j2)]++;
+      }
+    }
+    for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci) {
+      const PlanCol& pc = P.cols[size_t(ci)];
+      if ((pc.info >> 30) & 1) continue;   // fix-up
+      if ((pc.info >> 8) & 1) rstore[size_t(pc.c)]++; else rred[size_t(pc.c)]++;
+    }
+  }
+  for (int32_t v : seen) if (v != 1) ++bad_elem;
+  int64_t bad_slot = 0;
+  for (int64_t c = 0; c < nk; ++c) {
+    const int64_t nc = m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)];
+    const int64_t self = std::lower_bound(m->nbr.begin() + m->nbr_ptr[size_t(c)],
+                                          m->nbr.begin() + m->nbr_ptr[size_t(c) + 1], int32_t(c)) -
+                         (m->nbr.begin() + m->nbr_ptr[size_t(c)]);
+    for (int64_t s = 0; s < nc; ++s) {
+      const int64_t e = m->nbr_ptr[size_t(c)] + s;
+      int st = store[size_t(e)], rd = red[size_t(e)];
+      if (multi[size_t(c)] && s == self) st += 1;   // the fix-up store
+      const bool ok = (st == 1 && rd == 0) || (st == 0 && rd >= 1 && zeroed[size_t(c)]) ||
+                      (st == 0 && rd == 0 && false);
+      // a slot no local triangle couples (part meshes: foreign coupling) is
+      // stored as zero by an interior pair or cleared by the zero fill
+      const bool empty_ok = st == 0 && rd == 0 && zeroed[size_t(c)];
+      if (!ok && !empty_ok) ++bad_slot;
+    }
+    int rs = rstore[size_t(c)] + (multi[size_t(c)] ? 1 : 0), rr = rred[size_t(c)];
+    if (!((rs == 1 && rr == 0) || (rs == 0 && rr >= 1 && zeroed[size_t(c)]))) ++bad_slot;
+  }
+  stats[0] = P.n_patches;
+  stats[1] = int64_t(P.pairs.size());
+  stats[2] = n_contrib;
+  stats[3] = int64_t(P.zero_cols.size());
+  stats[4] = int64_t(P.multi.size());
+  stats[5] = bad_slot;
+  stats[6] = bad_elem;
+  stats[7] = P.max_plan_bytes;
+  return FO_OK;
 }
 
 }  // namespace fo

@@ -78,6 +78,7 @@ _SIGS = {
     "fo_halo_info": [P, P, P, P],
     "fo_halo_plan_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P],
     "fo_part_graph_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P, P],
+    "fo_plan_check_host": [I64, P, I64, P, I32, P, I32, I32, P],
 }
 _VOID = ["fo_mesh_destroy", "fo_graph_destroy", "fo_halo_destroy"]
 
@@ -155,6 +156,19 @@ def graph_host(n_vert, tri, n_layers):
     check(lib().fo_graph_host(n_vert, n_tri, _ptr(tri), n_layers, _ptr(row_ptr), _ptr(col), C.byref(nnz)),
           "fo_graph_host")
     return row_ptr, col
+
+
+def plan_check_host(xy, tri, n_layers, part=None, n_parts=1, my_part=0):
+    """host-only coverage check of the owner-computes plan (no device): dict of
+    patches, pairs, contributions, zero_cols, multi, bad_slots, bad_entries, plan_bytes."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    st = np.zeros(8, dtype=np.int64)
+    pt = None if part is None else np.ascontiguousarray(part, dtype=np.int32)
+    check(lib().fo_plan_check_host(xy.shape[0], _ptr(xy), tri.shape[0], _ptr(tri), n_layers, _ptr(pt),
+                                   my_part, n_parts, _ptr(st)), "fo_plan_check_host")
+    keys = ["patches", "pairs", "contributions", "zero_cols", "multi", "bad_slots", "bad_entries", "plan_bytes"]
+    return dict(zip(keys, st.tolist()))
 
 
 def part_graph_host(n_vert, tri, n_layers, part, n_parts, my_part):
