@@ -55,8 +55,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra, "-Xcompiler", "-fPIC",
                "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",
                "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
-        if src.endswith(".cpp"):
+        if src.endswith(".cpp"):   # host code: the -D switches of FO_EXTRA_NVCC_FLAGS apply too
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall",
+                   *[f for f in extra if f.startswith("-D")],
                    "-I", os.path.join(ROOT, "include"), "-I", inc,
                    "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include"),
                    "-c", src, "-o", obj]

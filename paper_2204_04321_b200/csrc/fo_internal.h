@@ -38,10 +38,18 @@ struct alignas(8) QuadRec {
 
 // Triangles per patch of the owner-computes kernel (one thread per triangle
 // column, 99 fp64 of shared memory per triangle).
+#ifdef FO_EXPERIMENT_PATCH255
+constexpr int kPatchTris = 255;
+#else
 constexpr int kPatchTris = 128;
+#endif
 // CTAs resident per SM (2: one CTA's gather phase overlaps the other's
 // element phase)
+#ifdef FO_EXPERIMENT_PATCH255
+constexpr int kPatchCtasPerSm = 1;
+#else
 constexpr int kPatchCtasPerSm = 2;
+#endif
 // row stride (doubles) of the [entry][triangle] shared-memory arrays: odd, so
 // entries of one triangle fall in different banks
 constexpr int kPatchStride = kPatchTris + 1;
