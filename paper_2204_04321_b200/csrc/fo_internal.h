@@ -76,12 +76,13 @@ struct MultiRec {           // 24 bytes
 };
 // doubles per (partial block, level): dg 4, up 4, nx 4, residual 2 (+2 pad)
 constexpr int kPartialStride = 16;
-struct PlanPair {           // 8 bytes: one (column, slot) of phase B
-  uint16_t off;             // first contribution (patch-relative)
-  uint8_t cnt;              // number of contributions
+struct alignas(16) PlanPair {   // 16 bytes: one (column, slot) of phase B
+  uint16_t off;             // contributions 2 .. cnt-1 (patch-relative index)
+  uint8_t cnt;              // number of contributions (even, >= 2)
   uint8_t slot;             // slot in the column's coupling list
   uint16_t col;             // patch-local column record
   uint16_t pad;
+  uint32_t c0, c1;          // contributions 0 and 1, inline (an edge pair's whole list)
 };
 
 // Work decomposition of the owner-computes kernel.

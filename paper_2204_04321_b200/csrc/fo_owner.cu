@@ -118,31 +118,42 @@ struct PairSums {
   double dg[4], up[4], nx[4];
 };
 
-// add the two contributions c2 (one gather step) to s
-template <bool UP>
+// one gather step over the two contributions c2: FIRST sets s = a + b (the
+// same double as (0 + a) + b, one add fewer), later steps add a, then b
+template <bool UP, bool FIRST>
 __device__ __forceinline__ void gather2(uint2 c2, const double* D, const double* O, PairSums& s) {
+  const int tla = int(c2.x & 255), tlb = int(c2.y & 255);
+  const int pata = int((c2.x >> 13) & 3), patb = int((c2.y >> 13) & 3);
+  const int saa = pata == 1 ? 2 * TP : TP, sba = pata == 2 ? 2 * TP : TP;
+  const int sab = patb == 1 ? 2 * TP : TP, sbb = patb == 2 ? 2 * TP : TP;
+  const double* Da = D + int((c2.x >> 8) & 31) * TP + tla;
+  const double* Db = D + int((c2.y >> 8) & 31) * TP + tlb;
+  if (FIRST) {
+    s.dg[0] = Da[0] + Db[0];
+    s.dg[1] = Da[sba] + Db[sbb];
+    s.dg[2] = Da[saa] + Db[sab];
+    s.dg[3] = Da[saa + sba] + Db[sab + sbb];
+  } else {
+    s.dg[0] = (s.dg[0] + Da[0]) + Db[0];
+    s.dg[1] = (s.dg[1] + Da[sba]) + Db[sbb];
+    s.dg[2] = (s.dg[2] + Da[saa]) + Db[sab];
+    s.dg[3] = (s.dg[3] + Da[saa + sba]) + Db[sab + sbb];
+  }
+  if (UP) {
+    const double* Oua = O + int((c2.x >> 15) & 31) * TP + tla;
+    const double* Ona = O + int((c2.x >> 20) & 31) * TP + tla;
+    const double* Oub = O + int((c2.y >> 15) & 31) * TP + tlb;
+    const double* Onb = O + int((c2.y >> 20) & 31) * TP + tlb;
+    constexpr int ou[4] = {0, TP, 6 * TP, 7 * TP}, on[4] = {0, 6 * TP, TP, 7 * TP};
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t cb = h ? c2.y : c2.x;
-    const int tl = int(cb & 255);
-    const int pat = int((cb >> 13) & 3);
-    const int sa = pat == 1 ? 2 * TP : TP, sb = pat == 2 ? 2 * TP : TP;
-    const double* Dt = D + int((cb >> 8) & 31) * TP + tl;
-    s.dg[0] += Dt[0];
-    s.dg[1] += Dt[sb];
-    s.dg[2] += Dt[sa];
-    s.dg[3] += Dt[sa + sb];
-    if (UP) {
-      const double* Ou = O + int((cb >> 15) & 31) * TP + tl;
-      const double* On = O + int((cb >> 20) & 31) * TP + tl;
-      s.up[0] += Ou[0];
-      s.up[1] += Ou[TP];
-      s.up[2] += Ou[6 * TP];
-      s.up[3] += Ou[7 * TP];
-      s.nx[0] += On[0];
-      s.nx[1] += On[6 * TP];
-      s.nx[2] += On[TP];
-      s.nx[3] += On[7 * TP];
+    for (int i = 0; i < 4; ++i) {
+      if (FIRST) {
+        s.up[i] = Oua[ou[i]] + Oub[ou[i]];
+        s.nx[i] = Ona[on[i]] + Onb[on[i]];
+      } else {
+        s.up[i] = (s.up[i] + Oua[ou[i]]) + Oub[ou[i]];
+        s.nx[i] = (s.nx[i] + Ona[on[i]]) + Onb[on[i]];
+      }
     }
   }
 }
@@ -198,10 +209,12 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
     PairSums s;
-    zero_sums(s);
-    const uint32_t* cp = sp.contrib + pp.off;   // even count, 8-byte aligned
+    const uint32_t* cp = sp.contrib + pp.off - 2;   // even count >= 2, 8-byte aligned
 #ifndef FO_EXPERIMENT_NO_GATHER
-    for (int e = 0; e < pp.cnt; e += 2) gather2<UP>(*reinterpret_cast<const uint2*>(cp + e), D, O, s);
+    gather2<UP, true>(make_uint2(pp.c0, pp.c1), D, O, s);
+    for (int e = 2; e < pp.cnt; e += 2) gather2<UP, false>(*reinterpret_cast<const uint2*>(cp + e), D, O, s);
+#else
+    zero_sums(s);
 #endif
     emit<UP>(pp, sp.cols[pp.col], s, kk, L, vals, partials);
   }
@@ -211,8 +224,15 @@ __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, con
                                           double* __restrict__ R, double* __restrict__ partials) {
   for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
     const PlanCol& pc = sp.cols[ci];
-    double r0 = 0.0, r1 = 0.0;
-    for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; e += 2) {
+    double r0, r1;
+    {   // self lists hold >= 2 entries (padded to even): first step r = a + b
+      const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + pc.self_off);
+      const double* Da = D + (21 + 2 * int((c2.x >> 25) & 3)) * TP + int(c2.x & 255);
+      const double* Db = D + (21 + 2 * int((c2.y >> 25) & 3)) * TP + int(c2.y & 255);
+      r0 = Da[0] + Db[0];
+      r1 = Da[TP] + Db[TP];
+    }
+    for (int e = pc.self_off + 2; e < pc.self_off + pc.self_cnt; e += 2) {
       const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + e);
       const double* Da = D + (21 + 2 * int((c2.x >> 25) & 3)) * TP + int(c2.x & 255);
       const double* Db = D + (21 + 2 * int((c2.y >> 25) & 3)) * TP + int(c2.y & 255);
@@ -329,13 +349,18 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
     const int64_t b0 = __ldg(pv.blob_off + p), b1 = __ldg(pv.blob_off + p + 1);
     char* base = reinterpret_cast<char*>(smem) + kPlanOffset;
-    sp.cols = reinterpret_cast<const PlanCol*>(base);
-    sp.pairs = reinterpret_cast<const PlanPair*>(base + (c1 - c0) * sizeof(PlanCol));
+    sp.pairs = reinterpret_cast<const PlanPair*>(base);
+    sp.cols = reinterpret_cast<const PlanCol*>(base + (q1 - q0) * sizeof(PlanPair));
     sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
     sp.ncols = c1 - c0; sp.npairs = q1 - q0;
     sp.nedge = __ldg(pv.nedge + p);
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
+#ifdef FO_STAGGER_NS
+  // experiment: the second CTA of each SM in the first wave starts late, so
+  // the two resident CTAs alternate their element and gather phases
+  if (blockIdx.x >= 148 && blockIdx.x < 296) __nanosleep(FO_STAGGER_NS);
+#endif
   const int L = kp.L;
   const int tl = threadIdx.x;
   const bool active = tl < nt;

@@ -105,18 +105,25 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
       if (l.size() & 1) l.push_back(uint32_t(kPatchTris));
       if (s != self && (interior || !l.empty()))   // edge slots: exactly two entries
         while (l.size() < 2) l.push_back(uint32_t(kPatchTris));   // (interior slots of a part mesh may have none)
-      if (s == self) {
-        pc.self_off = uint16_t(B.contrib.size());
-        pc.self_cnt = uint16_t(l.size());
-      }
       if (l.empty() && !interior) continue;   // boundary: only touched slots
       PlanPair pp{};
-      pp.off = uint16_t(B.contrib.size());
       pp.cnt = uint8_t(l.size());
       pp.slot = uint8_t(s);
       pp.col = uint16_t(ci);
-      if (s == self) self_pairs.push_back(pp); else B.pairs.push_back(pp);
-      B.contrib.insert(B.contrib.end(), l.begin(), l.end());
+      pp.c0 = l[0];   // the first two contributions inline: one 16-byte
+      pp.c1 = l[1];   // shared load gives an edge pair's whole list
+      if (s == self) {
+        // the self list is kept whole for the residual gather (phase_b_r)
+        pc.self_off = uint16_t(B.contrib.size());
+        pc.self_cnt = uint16_t(l.size());
+        pp.off = uint16_t(B.contrib.size() + 2);
+        B.contrib.insert(B.contrib.end(), l.begin(), l.end());
+        self_pairs.push_back(pp);
+      } else {
+        pp.off = uint16_t(B.contrib.size());
+        B.contrib.insert(B.contrib.end(), l.begin() + 2, l.end());
+        B.pairs.push_back(pp);
+      }
     }
     B.cols.push_back(pc);
     i = e;
@@ -184,8 +191,10 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
       P.cols.insert(P.cols.end(), B.cols.begin(), B.cols.end());
       P.pairs.insert(P.pairs.end(), B.pairs.begin(), B.pairs.end());
       P.contrib.insert(P.contrib.end(), B.contrib.begin(), B.contrib.end());
-      for (int32_t q = 0; q < B.nedge; ++q)   // an edge joins <= 2 triangles: padded to 2
-        if (B.pairs[size_t(q)].cnt != 2) return FO_EINVAL;
+      for (int32_t q = 0; q < int32_t(B.pairs.size()); ++q)   // an edge joins <= 2 triangles: padded to 2
+        if ((q < B.nedge && B.pairs[size_t(q)].cnt != 2) || B.pairs[size_t(q)].cnt < 2 ||
+            (B.pairs[size_t(q)].cnt & 1))
+          return FO_EINVAL;
       P.nedge.push_back(B.nedge);
       P.col_ptr.push_back(int32_t(P.cols.size()));
       P.pair_ptr.push_back(int32_t(P.pairs.size()));
@@ -225,7 +234,8 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
     P.n_partials = nb;
   }
   // one 16-byte aligned blob per patch in the shared-memory layout of the
-  // kernel (columns | pairs | contributions), copied with one bulk copy
+  // kernel (pairs | columns | contributions: the 16-byte pair records first,
+  // so they stay 16-byte aligned), copied with one bulk copy
   std::vector<uint8_t> blob;
   std::vector<int64_t> blob_off(1, 0);
   for (int32_t p = 0; p < P.n_patches; ++p) {
@@ -233,9 +243,9 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
       const uint8_t* b = static_cast<const uint8_t*>(src);
       blob.insert(blob.end(), b, b + n);
     };
-    put(P.cols.data() + P.col_ptr[size_t(p)], sizeof(PlanCol) * size_t(P.col_ptr[size_t(p) + 1] - P.col_ptr[size_t(p)]));
     put(P.pairs.data() + P.pair_ptr[size_t(p)],
         sizeof(PlanPair) * size_t(P.pair_ptr[size_t(p) + 1] - P.pair_ptr[size_t(p)]));
+    put(P.cols.data() + P.col_ptr[size_t(p)], sizeof(PlanCol) * size_t(P.col_ptr[size_t(p) + 1] - P.col_ptr[size_t(p)]));
     put(P.contrib.data() + P.contrib_ptr[size_t(p)],
         sizeof(uint32_t) * size_t(P.contrib_ptr[size_t(p) + 1] - P.contrib_ptr[size_t(p)]));
     blob.resize((blob.size() + 15) / 16 * 16, 0);
@@ -292,7 +302,8 @@ fo_status plan_check(const fo_mesh m, int64_t* stats) {
         red[size_t(e)]++;
       }
       for (int i = 0; i < pp.cnt; ++i) {
-        const uint32_t cb = P.contrib[size_t(P.contrib_ptr[size_t(p)] + pp.off + i)];
+        const uint32_t cb = i == 0 ? pp.c0 : i == 1 ? pp.c1
+                                    : P.contrib[size_t(P.contrib_ptr[size_t(p)] + pp.off + i - 2)];
         const int tl = int(cb & 255);
         if (tl == kPatchTris) continue;   // pad
         ++n_contrib;
