@@ -121,24 +121,51 @@ __device__ __forceinline__ double hex_jentry(const double G[8][3], const double 
   return fma(c, hh, -d * g[p] * g[p2]);
 }
 
-// add v0, v1 (column comps 0, 1) to row (node i, comp a) at column node i2
-__device__ __forceinline__ void hex_add(double* __restrict__ vals, const QuadRec& qr, const int64_t cs[4],
-                                        const int nc[4], int L, int k, int i, int a, int i2, double v0, double v1) {
+// position of the (column comps 0, 1) pair of row (node i, comp a) at column node i2
+__device__ __forceinline__ double2* hex_ptr(double* __restrict__ vals, const QuadRec& qr, const int64_t cs[4],
+                                            const int nc[4], int L, int k, int i, int a, int i2) {
   const int j = i & 3, ki = k + (i >> 2), j2 = i2 & 3, ki2 = k + (i2 >> 2);
   const int m = (ki == 0 || ki == L) ? 2 : 3;
   const int P = ki == 0 ? 0 : 3 * ki - 1;
   const int kmin = ki == 0 ? 0 : ki - 1;
-  double2* rr = reinterpret_cast<double2*>(vals + cs[j] + int64_t(4 * nc[j]) * P + int64_t(a) * 2 * nc[j] * m +
-                                           int(qr.slot[4 * j + j2]) * 2 * m + 2 * (ki2 - kmin));
-  const double2 o = *rr;
-  *rr = make_double2(o.x + v0, o.y + v1);
+  return reinterpret_cast<double2*>(vals + cs[j] + int64_t(4 * nc[j]) * P + int64_t(a) * 2 * nc[j] * m +
+                                    int(qr.slot[4 * j + j2]) * 2 * m + 2 * (ki2 - kmin));
+}
+
+// read-modify-write of N double2 targets with every load issued before the
+// first store: the targets are distinct (colouring), but the compiler cannot
+// prove it, and one RMW at a time waits a DRAM latency per target.
+// f(n, p, v0, v1) names target n and the values to add.
+#ifndef FO_HEX_RMW_BATCH
+#define FO_HEX_RMW_BATCH 8
+#endif
+constexpr int kRmw = FO_HEX_RMW_BATCH;   // block RMWs in flight per thread
+
+template <int N, class F>
+__device__ __forceinline__ void rmw_batch(F f) {
+  double2* p[N];
+  double v0[N], v1[N];
+  double2 o[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) f(n, p[n], v0[n], v1[n]);
+#pragma unroll
+  for (int n = 0; n < N; ++n) o[n] = *p[n];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+#ifdef FO_EXPERIMENT_HEX_NO_SCATTER   // keep the sums alive, store nothing
+    if (v0[n] == 1.2345e300 && v1[n] == -1.0) *p[n] = o[n];
+#else
+    *p[n] = make_double2(o[n].x + v0[n], o[n].y + v1[n]);
+#endif
+  }
 }
 
 // One thread per hexahedron; the 16 x 16 block is accumulated in registers in
 // three passes over the 8 points -- (bottom, bottom) with the residual and the
 // basal term, (bottom, top), (top, top) -- re-evaluating the point data in
 // each pass rather than keeping 136 accumulators live; after each pass the
-// block is added into the CSR values (both orientations, J symmetric).
+// block is added into the CSR values (both orientations, J symmetric), eight
+// read-modify-writes in flight at a time (rmw_batch).
 template <bool NEED_J, bool N3>
 __global__ void __launch_bounds__(kHexThreads)
 hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, const int32_t* __restrict__ ids,
@@ -236,29 +263,25 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double2* rr = reinterpret_cast<double2*>(R) + int64_t(qr.v[i & 3]) * (L + 1) + k + (i >> 2);
-    const double2 o = *rr;
-    *rr = make_double2(o.x + r[2 * i], o.y + r[2 * i + 1]);
-  }
+  rmw_batch<8>([&](int i, double2*& p, double& v0, double& v1) {
+    p = reinterpret_cast<double2*>(R) + int64_t(qr.v[i & 3]) * (L + 1) + k + (i >> 2);
+    v0 = r[2 * i];
+    v1 = r[2 * i + 1];
+  });
   if (!NEED_J) return;
   // (bottom, bottom): rows of bottom node i, columns of bottom node i2
+  auto sym = [](const double* blk, int p, int p2) {
+    const int lo = p < p2 ? p : p2, hi = p < p2 ? p2 : p;
+    return blk[lo * 8 - (lo * (lo - 1)) / 2 + (hi - lo)];
+  };
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int i2 = 0; i2 < 4; ++i2)
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        double v[2];
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int p = 2 * i + a, p2 = 2 * i2 + b;
-          const int lo = p < p2 ? p : p2, hi = p < p2 ? p2 : p;
-          v[b] = bb[lo * 8 - (lo * (lo - 1)) / 2 + (hi - lo)];
-        }
-        hex_add(vals, qr, cs, nc, L, k, i, a, i2, v[0], v[1]);
-      }
+  for (int c0 = 0; c0 < 32; c0 += kRmw)
+    rmw_batch<kRmw>([&](int n, double2*& p, double& v0, double& v1) {
+      const int e = c0 + n, i = e >> 3, i2 = (e >> 1) & 3, a = e & 1;
+      p = hex_ptr(vals, qr, cs, nc, L, k, i, a, i2);
+      v0 = sym(bb, 2 * i + a, 2 * i2);
+      v1 = sym(bb, 2 * i + a, 2 * i2 + 1);
+    });
   // ---- pass 2: (bottom, top) block; written for both orientations
   {
     double bt[64];
@@ -275,16 +298,19 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
         for (int p2 = 0; p2 < 8; ++p2) bt[8 * p + p2] += hex_jentry(G, g, c, d, p, 8 + p2);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2)
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          // row bottom node i, column top node 4 + i2
-          hex_add(vals, qr, cs, nc, L, k, i, a, 4 + i2, bt[8 * (2 * i + a) + 2 * i2], bt[8 * (2 * i + a) + 2 * i2 + 1]);
-          // row top node 4 + i2, column bottom node i (transpose)
-          hex_add(vals, qr, cs, nc, L, k, 4 + i2, a, i, bt[8 * (2 * i) + 2 * i2 + a], bt[8 * (2 * i + 1) + 2 * i2 + a]);
+    for (int c0 = 0; c0 < 64; c0 += kRmw)
+      rmw_batch<kRmw>([&](int n, double2*& p, double& v0, double& v1) {
+        const int e = c0 + n, i = e >> 4, i2 = (e >> 2) & 3, a = (e >> 1) & 1;
+        if ((e & 1) == 0) {   // row bottom node i, column top node 4 + i2
+          p = hex_ptr(vals, qr, cs, nc, L, k, i, a, 4 + i2);
+          v0 = bt[8 * (2 * i + a) + 2 * i2];
+          v1 = bt[8 * (2 * i + a) + 2 * i2 + 1];
+        } else {              // row top node 4 + i2, column bottom node i (transpose)
+          p = hex_ptr(vals, qr, cs, nc, L, k, 4 + i2, a, i);
+          v0 = bt[8 * (2 * i) + 2 * i2 + a];
+          v1 = bt[8 * (2 * i + 1) + 2 * i2 + a];
         }
+      });
   }
   // ---- pass 3: (top, top) block
   {
@@ -303,20 +329,13 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
         for (int p2 = p; p2 < 8; ++p2) tt[e++] += hex_jentry(G, g, c, d, 8 + p, 8 + p2);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2)
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          double v[2];
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const int p = 2 * i + a, p2 = 2 * i2 + b;
-            const int lo = p < p2 ? p : p2, hi = p < p2 ? p2 : p;
-            v[b] = tt[lo * 8 - (lo * (lo - 1)) / 2 + (hi - lo)];
-          }
-          hex_add(vals, qr, cs, nc, L, k, 4 + i, a, 4 + i2, v[0], v[1]);
-        }
+    for (int c0 = 0; c0 < 32; c0 += kRmw)
+      rmw_batch<kRmw>([&](int n, double2*& p, double& v0, double& v1) {
+        const int e = c0 + n, i = e >> 3, i2 = (e >> 1) & 3, a = e & 1;
+        p = hex_ptr(vals, qr, cs, nc, L, k, 4 + i, a, 4 + i2);
+        v0 = sym(tt, 2 * i + a, 2 * i2);
+        v1 = sym(tt, 2 * i + a, 2 * i2 + 1);
+      });
   }
 }
 

@@ -40,6 +40,23 @@ struct PlanView {
   double* partials;   // multi columns' partial blocks (fo_plan.cpp)
 };
 
+#ifdef FO_TRACE
+// experiment: per-patch %globaltimer stamps (smid, start, then the end of
+// every phase A and phase B), read back by fo_debug_trace (tools/trace_phases.py)
+constexpr int kTraceSlots = 24, kTraceMax = 8192;
+__device__ unsigned long long g_trace[kTraceMax * kTraceSlots];
+__device__ __forceinline__ void trace(int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax && slot < kTraceSlots) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x * kTraceSlots + slot] = t;
+  }
+}
+#define FO_TRACE_AT(s) trace(s)
+#else
+#define FO_TRACE_AT(s)
+#endif
+
 // one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor)
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
@@ -361,6 +378,14 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   // the two resident CTAs alternate their element and gather phases
   if (blockIdx.x >= 148 && blockIdx.x < 296) __nanosleep(FO_STAGGER_NS);
 #endif
+#ifdef FO_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[blockIdx.x * kTraceSlots] = smid;
+  }
+  FO_TRACE_AT(1);
+#endif
   const int L = kp.L;
   const int tl = threadIdx.x;
   const bool active = tl < nt;
@@ -397,10 +422,12 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     }
     if (k == 0) bulk_wait(&plan_bar);
     __syncthreads();
+    FO_TRACE_AT(2 + 2 * k);
 #ifndef FO_EXPERIMENT_NO_PHASE_B
     phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials);
 #endif
     __syncthreads();
+    FO_TRACE_AT(3 + 2 * k);
     if (active) {   // the held top block becomes level k+1's diagonal block
       if (NEED_J) {
 #pragma unroll
@@ -414,6 +441,10 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   if (L == 0) bulk_wait(&plan_bar);
   __syncthreads();
   phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials);
+#ifdef FO_TRACE
+  __syncthreads();
+  FO_TRACE_AT(2 + 2 * L);
+#endif
 }
 
 // zero the rows (CSR values and residual) of boundary columns
@@ -562,3 +593,10 @@ fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals
 }
 
 }  // namespace fo
+
+#ifdef FO_TRACE
+extern "C" __attribute__((visibility("default"))) int fo_debug_trace(unsigned long long* host, long n) {
+  if (n > long(fo::kTraceMax) * fo::kTraceSlots) n = long(fo::kTraceMax) * fo::kTraceSlots;
+  return int(cudaMemcpyFromSymbol(host, fo::g_trace, size_t(n) * 8));
+}
+#endif
