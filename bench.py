@@ -347,10 +347,21 @@ def main():
             "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
             "bytes_formula": "8 nnz + 32 N_nodes + 40 N_cols + 12 N_tri (SURVEY.md 8(d) d3)"}
     if fp64:
-        roof["fp64"] = fp64
-        # the binding roof is the larger floor (FP64 here)
-        roof["min_roof"] = {"binding": "fp64" if fp64["frac"] > roof["frac"] else "hbm",
-                            "frac": max(fp64["frac"], roof["frac"])}
+        # the binding roof is the larger floor.  When it is
+        # the FP64 pipe (plain fp64 ALU arithmetic, no tensor cores: DESIGN.md
+        # section 7), the line reports "bound": "alu" against the derived FP64
+        # peak and keeps the metric's HBM fraction under "hbm".
+        binding = "fp64" if fp64["frac"] > roof["frac"] else "hbm"
+        roof["min_roof"] = {"binding": binding, "frac": max(fp64["frac"], roof["frac"])}
+        if binding == "fp64":
+            hbm = {k: roof.pop(k) for k in ("achieved", "peak", "unit", "frac", "peak_source", "bytes_formula",
+                                            "algorithmic_bytes_per_launch")}
+            roof = {"bound": "alu", "achieved": fp64["achieved"], "peak": fp64["peak"], "unit": "TFLOP/s",
+                    "frac": fp64["frac"], "traffic": roof.pop("traffic"), **roof,
+                    "flop_per_wedge": fp64["flop_per_wedge"], "peak_source": fp64["peak_source"],
+                    "flop_source": fp64["flop_source"], "hbm": hbm}
+        else:
+            roof["fp64"] = fp64
     if prof:
         roof["ncu"] = {k: prof.get(k) for k in ("fp64_pipe_pct", "registers_per_thread", "warps_active_pct",
                                                  "l1_data_pipe_pct", "shared_wavefronts", "shared_bank_conflicts",

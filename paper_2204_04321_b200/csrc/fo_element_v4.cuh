@@ -42,6 +42,27 @@
 
 namespace fo {
 
+// (x)^(-1/3) for the n = 3 viscosity: an fp32 seed from the SFU
+// (log2 / exp2, relative error ~1e-6) and two Newton steps y <- y (4 - x y^3) / 3
+// in fp64 (error ~2 e^2 per step: 1e-6 -> 2e-12 -> 1e-23, i.e. correctly
+// rounded up to an ulp); x = q + eps_reg >= eps_reg > 0 lies in the fp32
+// normal range.  Fewer issue slots than the libdevice rcbrt (FO_LIBDEVICE_RCBRT).
+__device__ __forceinline__ double rcbrt_n3(double x) {
+#ifdef FO_LIBDEVICE_RCBRT
+  return rcbrt(x);
+#else
+  const float xf = __double2float_rn(x);
+  double y = double(exp2f(-0.333333343f * __log2f(xf)));
+  constexpr double k43 = 4.0 / 3.0, k13 = 1.0 / 3.0;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double t = x * y * y * y;
+    y = y * fma(-k13, t, k43);
+  }
+  return y;
+#endif
+}
+
 __host__ __device__ constexpr int pk6(int p, int q) {
   return p <= q ? p * 6 - (p * (p - 1)) / 2 + (q - p) : q * 6 - (q * (q - 1)) / 2 + (p - q);
 }
@@ -182,7 +203,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       const double W = W0 * (a == 0 ? zz[0] : (a == 1 ? zz[1] : zz[2]));
       double c, d;
       if (N3) {
-        const double y = rcbrt(qe[q]);               // (q + eps)^(-1/3)
+        const double y = rcbrt_n3(qe[q]);            // (q + eps)^(-1/3)
         c = W * w.Afac * y;                           // w_q 2 mu_q
         d = c * (y * y * y) * (1.0 / 3.0);            // c (n-1)/(2n) / (q+eps)
       } else {
