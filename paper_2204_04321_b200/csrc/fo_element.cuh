@@ -30,6 +30,42 @@ namespace fo {
 
 __host__ __device__ constexpr int jidx(int p, int q) { return p * 12 - (p * (p - 1)) / 2 + (q - p); }
 
+// (x)^(-1/3) for the n = 3 viscosity: an fp32 seed from the SFU
+// (log2 / exp2, relative error ~1e-6) and two Newton steps y <- y (4 - x y^3) / 3
+// in fp64 (error ~2 e^2 per step: 1e-6 -> 2e-12 -> 1e-23, i.e. correctly
+// rounded up to an ulp); x = q + eps_reg >= eps_reg > 0 lies in the fp32
+// normal range.  Fewer issue slots than the libdevice rcbrt (FO_LIBDEVICE_RCBRT).
+__device__ __forceinline__ double rcbrt_n3(double x) {
+#ifdef FO_LIBDEVICE_RCBRT
+  return rcbrt(x);
+#else
+  const float xf = __double2float_rn(x);
+  double y = double(exp2f(-0.333333343f * __log2f(xf)));
+  constexpr double k43 = 4.0 / 3.0, k13 = 1.0 / 3.0;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double t = x * y * y * y;
+    y = y * fma(-k13, t, k43);
+  }
+  return y;
+#endif
+}
+
+// 1/x for the geometry's reciprocals (x != 0, |x| in the fp32 normal range: a
+// layer's vertical half-height in metres, twice a footprint triangle's area in
+// m^2): fp32 SFU seed (relative error ~1e-7) and two Newton steps
+// y <- y + y (1 - x y) (1e-7 -> 1e-14 -> 1e-28), no slow-path branches.
+__device__ __forceinline__ double rcp_geo(double x) {
+#ifdef FO_LIBDEVICE_RCBRT
+  return 1.0 / x;
+#else
+  double y = double(__frcp_rn(__double2float_rn(x)));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+#endif
+}
+
 struct WedgeIn {
   double a[3], b[3];   // footprint gradients of the barycentrics
   double D;            // 2 |T|

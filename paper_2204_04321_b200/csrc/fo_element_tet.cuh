@@ -109,7 +109,7 @@ __device__ __forceinline__ void tet3_element(const WedgeIn& w, int order, double
     const double qe = qq + eps;
     double c, d;
     if (N3) {
-      const double y = rcbrt(qe);
+      const double y = rcbrt_n3(qe);
       c = vol * w.Afac * y;
       d = c * (y * y * y) * (1.0 / 3.0);
     } else {

@@ -42,27 +42,6 @@
 
 namespace fo {
 
-// (x)^(-1/3) for the n = 3 viscosity: an fp32 seed from the SFU
-// (log2 / exp2, relative error ~1e-6) and two Newton steps y <- y (4 - x y^3) / 3
-// in fp64 (error ~2 e^2 per step: 1e-6 -> 2e-12 -> 1e-23, i.e. correctly
-// rounded up to an ulp); x = q + eps_reg >= eps_reg > 0 lies in the fp32
-// normal range.  Fewer issue slots than the libdevice rcbrt (FO_LIBDEVICE_RCBRT).
-__device__ __forceinline__ double rcbrt_n3(double x) {
-#ifdef FO_LIBDEVICE_RCBRT
-  return rcbrt(x);
-#else
-  const float xf = __double2float_rn(x);
-  double y = double(exp2f(-0.333333343f * __log2f(xf)));
-  constexpr double k43 = 4.0 / 3.0, k13 = 1.0 / 3.0;
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double t = x * y * y * y;
-    y = y * fma(-k13, t, k43);
-  }
-  return y;
-#endif
-}
-
 __host__ __device__ constexpr int pk6(int p, int q) {
   return p <= q ? p * 6 - (p * (p - 1)) / 2 + (q - p) : q * 6 - (q * (q - 1)) / 2 + (p - q);
 }
@@ -104,7 +83,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       zz[a] = (3.0 * h[a] + hs) * kSixth;           // z_zeta at triangle point a
-      const double izz = 1.0 / zz[a];
+      const double izz = rcp_geo(zz[a]);
       rho[a] = 0.5 * izz;                           // r_j(a) = L_j(a) rho_a
       uz[a] = (3.0 * du[a] + dus) * kSixth * izz;   // u_z at point a
       vz[a] = (3.0 * dv[a] + dvs) * kSixth * izz;
@@ -336,19 +315,30 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
               sink.top(pk6(p, p2), hpart(ca, j, 1, cb, j2, 1));
               sink.bot_add(p, p2, hpart(ca, j, 0, cb, j2, 0));
             }
+#ifndef FO_H_BT_IN_REGS
             const double v = hpart(ca, j, 0, cb, j2, 1);
             sink.off(p, p2, v);
             gate = v;
             if (j != j2) sink.off(p2, p, hpart(cb, j2, 0, ca, j, 1));
+#else
+            gate = sink.top_get(pk6(p <= p2 ? p : p2, p <= p2 ? p2 : p));
+#endif
           }
       }
   }
   if (w.go) {   // rank-1 (bottom, top), accumulated onto the frozen-viscosity part
     double acc[36];
+#ifndef FO_H_BT_IN_REGS
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
       for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
+#else   // the (bottom, top) frozen-viscosity part straight into the accumulators
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = fma(0.0, gate, hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 1));
+#endif
 FO_UNROLL(FO_UNROLL_R1A)
     for (int q = 0; q < 6; ++q) {   // rolled: not all six points' data live at once
       const int a = q >> 1;

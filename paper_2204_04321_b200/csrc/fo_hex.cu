@@ -92,7 +92,7 @@ __device__ __forceinline__ void hex_visc(const HexIn& h, const double G[8][3], d
   const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
   const double qe = qq + kp.eps;
   if (N3) {
-    const double y = rcbrt(qe);
+    const double y = rcbrt_n3(qe);
     c = W * h.Afac * y;
     d = c * (y * y * y) * (1.0 / 3.0);
   } else {

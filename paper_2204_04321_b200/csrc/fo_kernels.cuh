@@ -75,7 +75,7 @@ __device__ __forceinline__ void load_tri_geo(const ColRec* __restrict__ col, con
   g.e1x = x[1] - x[0]; g.e1y = y[1] - y[0];
   g.e2x = x[2] - x[0]; g.e2y = y[2] - y[0];
   g.D = g.e1x * g.e2y - g.e2x * g.e1y;
-  const double iD = 1.0 / g.D;
+  const double iD = rcp_geo(g.D);
   g.a[0] = (g.e1y - g.e2y) * iD; g.a[1] = g.e2y * iD; g.a[2] = -g.e1y * iD;
   g.b[0] = (g.e2x - g.e1x) * iD; g.b[1] = -g.e2x * iD; g.b[2] = g.e1x * iD;
   g.sx = g.a[0] * s[0] + g.a[1] * s[1] + g.a[2] * s[2];
