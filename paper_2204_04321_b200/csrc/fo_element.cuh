@@ -40,7 +40,10 @@ __device__ __forceinline__ double rcbrt_n3(double x) {
   return rcbrt(x);
 #else
   const float xf = __double2float_rn(x);
-  double y = double(exp2f(-0.333333343f * __log2f(xf)));
+  float l2, yf;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(xf));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(-0.333333343f * l2));
+  double y = double(yf);
   constexpr double k43 = 4.0 / 3.0, k13 = 1.0 / 3.0;
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
@@ -59,7 +62,9 @@ __device__ __forceinline__ double rcp_geo(double x) {
 #ifdef FO_LIBDEVICE_RCBRT
   return 1.0 / x;
 #else
-  double y = double(__frcp_rn(__double2float_rn(x)));
+  float yf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(__double2float_rn(x)));
+  double y = double(yf);
 #pragma unroll
   for (int it = 0; it < 2; ++it) y = fma(y, fma(-x, y, 1.0), y);
   return y;
