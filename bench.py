@@ -356,6 +356,7 @@ def main():
         if binding == "fp64":
             hbm = {k: roof.pop(k) for k in ("achieved", "peak", "unit", "frac", "peak_source", "bytes_formula",
                                             "algorithmic_bytes_per_launch")}
+            roof.pop("bound")
             roof = {"bound": "alu", "achieved": fp64["achieved"], "peak": fp64["peak"], "unit": "TFLOP/s",
                     "frac": fp64["frac"], "traffic": roof.pop("traffic"), **roof,
                     "flop_per_wedge": fp64["flop_per_wedge"], "peak_source": fp64["peak_source"],

@@ -82,6 +82,11 @@ constexpr int kC = 36;   // compact per-point scratch (6 x 6 quadrature points)
 constexpr int kSlotsPerTri = kD + kO + kC;
 // byte offset of the plan in dynamic shared memory (16-byte aligned for the bulk copy)
 constexpr int kPlanOffset = (kSlotsPerTri * TP * 8 + 15) / 16 * 16;
+// residual only (KR): the residual slots of D (6) and the compact scratch, so
+// three CTAs fit an SM (shared memory and <= 168 registers)
+constexpr int kDR = 6;
+constexpr int kPlanOffsetR = ((kDR + kC) * TP * 8 + 15) / 16 * 16;
+constexpr int kPatchCtasPerSmR = 3;
 
 // D layout: the three off-diagonal 2x2 node blocks (j < j2) first, row-major
 // [a][b], at 4 (j + j2 - 1); then the three diagonal node blocks (a <= b) at
@@ -223,8 +228,17 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
   // edge pairs (exactly two entries) first, then self pairs (one entry per
   // fan triangle, padded to even); a variant gathering two edge pairs per
   // thread at a time measured slower (1.98 vs 1.91 ms)
+#ifdef FO_PB_PREFETCH
+  // the next pair's record is loaded while this pair gathers and stores
+  PlanPair nxt;
+  if (int(threadIdx.x) < sp.npairs) nxt = sp.pairs[threadIdx.x];
+  for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
+    const PlanPair pp = nxt;
+    if (pi + int(blockDim.x) < sp.npairs) nxt = sp.pairs[pi + blockDim.x];
+#else
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
+#endif
     PairSums s;
     const uint32_t* cp = sp.contrib + pp.off - 2;   // even count >= 2, 8-byte aligned
 #ifndef FO_EXPERIMENT_NO_GATHER
@@ -237,22 +251,23 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
   }
 }
 
-__device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, const double* D,
+// Dr: the residual slots (D + 21 TP in the R + J layout, the whole D of KR)
+__device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, const double* Dr,
                                           double* __restrict__ R, double* __restrict__ partials) {
   for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
     const PlanCol& pc = sp.cols[ci];
     double r0, r1;
     {   // self lists hold >= 2 entries (padded to even): first step r = a + b
       const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + pc.self_off);
-      const double* Da = D + (21 + 2 * int((c2.x >> 25) & 3)) * TP + int(c2.x & 255);
-      const double* Db = D + (21 + 2 * int((c2.y >> 25) & 3)) * TP + int(c2.y & 255);
+      const double* Da = Dr + 2 * int((c2.x >> 25) & 3) * TP + int(c2.x & 255);
+      const double* Db = Dr + 2 * int((c2.y >> 25) & 3) * TP + int(c2.y & 255);
       r0 = Da[0] + Db[0];
       r1 = Da[TP] + Db[TP];
     }
     for (int e = pc.self_off + 2; e < pc.self_off + pc.self_cnt; e += 2) {
       const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + e);
-      const double* Da = D + (21 + 2 * int((c2.x >> 25) & 3)) * TP + int(c2.x & 255);
-      const double* Db = D + (21 + 2 * int((c2.y >> 25) & 3)) * TP + int(c2.y & 255);
+      const double* Da = Dr + 2 * int((c2.x >> 25) & 3) * TP + int(c2.x & 255);
+      const double* Db = Dr + 2 * int((c2.y >> 25) & 3) * TP + int(c2.y & 255);
       r0 += Da[0];
       r1 += Da[TP];
       r0 += Db[0];
@@ -274,7 +289,7 @@ __device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const
     if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals, partials);
     else phase_b_j<false>(sp, kk, L, D, O, vals, partials);
   }
-  phase_b_r(sp, kk, L, D, R, partials);
+  phase_b_r(sp, kk, L, NEED_J ? D + 21 * TP : D, R, partials);
 }
 
 // Sink of wedge_element_v4: bottom parts added to D and O in shared memory,
@@ -319,12 +334,13 @@ struct PatchSink {
   __device__ __forceinline__ void r_top_add(int p, double v) { held[21 + p] += v; }
 };
 
-// residual-only sink: the Jacobian parts of the element are dead code
+// residual-only sink: the Jacobian parts of the element are dead code; D is
+// the compact KR layout (the 6 residual slots only)
 struct PatchSinkR {
   double* D;
   int tl;
   double held[27];
-  __device__ __forceinline__ void r_bot_add(int p, double v) { D[(21 + p) * TP + tl] += v; }
+  __device__ __forceinline__ void r_bot_add(int p, double v) { D[p * TP + tl] += v; }
   __device__ __forceinline__ void bot_add(int, int, double) {}
   __device__ __forceinline__ void off(int, int, double) {}
   __device__ __forceinline__ void off_add(int, int, double) {}
@@ -346,15 +362,15 @@ struct SmemCmp {
 };
 
 template <bool NEED_J, bool N3, bool TET>
-__global__ void __launch_bounds__(kPatchTris, kPatchCtasPerSm)
+__global__ void __launch_bounds__(kPatchTris, NEED_J ? kPatchCtasPerSm : kPatchCtasPerSmR)
 ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
                 const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp,
                 PlanView pv, const double* __restrict__ U, double* __restrict__ R,
                 double* __restrict__ vals) {
   extern __shared__ __align__(16) double smem[];
-  double* const D = smem;                    // [kD][TP]
-  double* const O = smem + kD * TP;          // [kO][TP]
-  double* const C = smem + (kD + kO) * TP;   // [kC][TP]
+  double* const D = smem;                                       // [kD][TP] (KR: [kDR][TP])
+  double* const O = smem + kD * TP;                             // [kO][TP] (KR: unused)
+  double* const C = smem + (NEED_J ? kD + kO : kDR) * TP;       // [kC][TP]
   const int p = blockIdx.x;
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   // the patch's plan -> shared memory (after the value buffers): one bulk
@@ -365,7 +381,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
     const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
     const int64_t b0 = __ldg(pv.blob_off + p), b1 = __ldg(pv.blob_off + p + 1);
-    char* base = reinterpret_cast<char*>(smem) + kPlanOffset;
+    char* base = reinterpret_cast<char*>(smem) + (NEED_J ? kPlanOffset : kPlanOffsetR);
     sp.pairs = reinterpret_cast<const PlanPair*>(base);
     sp.cols = reinterpret_cast<const PlanCol*>(base + (q1 - q0) * sizeof(PlanPair));
     sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
@@ -396,11 +412,11 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     const int2 v01 = __ldg(reinterpret_cast<const int2*>(tp));
     tr.v[0] = v01.x; tr.v[1] = v01.y; tr.v[2] = __ldg(tp + 2);
 #pragma unroll
-    for (int i = 0; i < kD; ++i) D[i * TP + tl] = 0.0;
+    for (int i = 0; i < (NEED_J ? kD : kDR); ++i) D[i * TP + tl] = 0.0;
   }
   // triangle slot kPatchTris: the zero column the plan's pad entries read
-  if (threadIdx.x < kD) D[threadIdx.x * TP + kPatchTris] = 0.0;
-  if (threadIdx.x < kO) O[threadIdx.x * TP + kPatchTris] = 0.0;
+  if (threadIdx.x < (NEED_J ? kD : kDR)) D[threadIdx.x * TP + kPatchTris] = 0.0;
+  if (NEED_J && threadIdx.x < kO) O[threadIdx.x * TP + kPatchTris] = 0.0;
   for (int k = 0; k < L; ++k) {
     typename std::conditional<NEED_J, PatchSink, PatchSinkR>::type sk;
     sk.D = D;
@@ -434,7 +450,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
         for (int i = 0; i < kD; ++i) D[i * TP + tl] = sk.held[i];
       } else {
 #pragma unroll
-        for (int i = 21; i < kD; ++i) D[i * TP + tl] = sk.held[i];
+        for (int i = 21; i < kD; ++i) D[(i - 21) * TP + tl] = sk.held[i];
       }
     }
   }
@@ -510,7 +526,7 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
   }
 }
 
-static size_t smem_bytes(bool) { return size_t(kPlanOffset) + kPlanBytes; }
+static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
 template <bool NEED_J, bool N3, bool TET>
 static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
