@@ -228,17 +228,8 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
   // edge pairs (exactly two entries) first, then self pairs (one entry per
   // fan triangle, padded to even); a variant gathering two edge pairs per
   // thread at a time measured slower (1.98 vs 1.91 ms)
-#ifdef FO_PB_PREFETCH
-  // the next pair's record is loaded while this pair gathers and stores
-  PlanPair nxt;
-  if (int(threadIdx.x) < sp.npairs) nxt = sp.pairs[threadIdx.x];
-  for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
-    const PlanPair pp = nxt;
-    if (pi + int(blockDim.x) < sp.npairs) nxt = sp.pairs[pi + blockDim.x];
-#else
   for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
     const PlanPair pp = sp.pairs[pi];
-#endif
     PairSums s;
     const uint32_t* cp = sp.contrib + pp.off - 2;   // even count >= 2, 8-byte aligned
 #ifndef FO_EXPERIMENT_NO_GATHER
