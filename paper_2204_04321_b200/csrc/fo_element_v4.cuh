@@ -170,8 +170,14 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         // strain-rate vectors
         const double e1x = 2.0 * ux + vy, e1y = exy, e1z = exz;
         const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
+#ifdef FO_QSCALED   // stored as rho_a Q / 6: r_j Q = (j == a ? 4 : 1) x the stored value
+        const double r6 = rho[a] * kSixth;
+        Qu(q) = (e1z - e1x * zx - e1y * zy) * r6;
+        Qv(q) = (e2z - e2x * zx - e2y * zy) * r6;
+#else
         Qu(q) = e1z - e1x * zx - e1y * zy;
         Qv(q) = e2z - e2x * zx - e2y * zy;
+#endif
         E1x(q) = e1x; E1y(q) = e1y; E2y(q) = e2y;   // e2x == e1y
       }
     }
@@ -291,6 +297,54 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       return fma(Fv, AA, fma(-sg, G1, fma(-sg2, G2, sg * sg2 * KKuv[kk])));
     }
   };
+#ifndef FO_HPART_SINGLE
+  // the four level blocks of one (row comp ca, node j; column comp cb, node
+  // j2) entry from shared pieces: entry(l, l2) = F_{l+l2} AA - s(l2) Rt(l)
+  // - s(l) Ct(l2) + s(l) s(l2) KK with s(0) = -1, s(1) = +1 (the terms of hpart)
+  auto hpart4 = [&](int ca, int j, int cb, int j2, double& e00, double& e01, double& e10, double& e11) {
+    const int kk = j <= j2 ? (j * 3 - (j * (j - 1)) / 2 + (j2 - j)) : (j2 * 3 - (j2 * (j2 - 1)) / 2 + (j - j2));
+    const double aj = w.a[j], bj = w.b[j], aj2 = w.a[j2], bj2 = w.b[j2];
+    double AA, KK, Rt[2], Ct[2];
+    if (ca == 0 && cb == 0) {
+      AA = fma(a2[j], aj2, bh[j] * bj2);
+      KK = KKuu[kk];
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        Rt[l] = fma(a2[j], T2x[l][j2], bh[j] * T2y[l][j2]);
+        Ct[l] = fma(a2[j2], T2x[l][j], bh[j2] * T2y[l][j]);
+      }
+    } else if (ca == 1 && cb == 1) {
+      AA = fma(ah[j], aj2, b2[j] * bj2);
+      KK = KKvv[kk];
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        Rt[l] = fma(ah[j], T2x[l][j2], b2[j] * T2y[l][j2]);
+        Ct[l] = fma(ah[j2], T2x[l][j], b2[j2] * T2y[l][j]);
+      }
+    } else if (ca == 0) {
+      AA = fma(aj, bj2, ah[j2] * bj);
+      KK = KKuv[kk];
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        Rt[l] = fma(aj, T2y[l][j2], bh[j] * T2x[l][j2]);
+        Ct[l] = fma(bj2, T2x[l][j], ah[j2] * T2y[l][j]);
+      }
+    } else {
+      AA = fma(aj2, bj, ah[j] * bj2);
+      KK = KKuv[kk];
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        Rt[l] = fma(bj, T2x[l][j2], ah[j] * T2y[l][j2]);
+        Ct[l] = fma(aj2, T2y[l][j], bh[j2] * T2x[l][j]);
+      }
+    }
+    const double X = fma(F[1], AA, -KK);
+    e01 = (X - Rt[0]) + Ct[1];
+    e10 = (X + Rt[1]) - Ct[0];
+    e00 = fma(F[0], AA, KK + (Rt[0] + Ct[0]));
+    e11 = fma(F[2], AA, KK - (Rt[1] + Ct[1]));
+  };
+#endif
   // The sections below are wrapped in `if (w.go)` (always true at run time):
   // branch boundaries keep ptxas from interleaving them, and each rank-1
   // block reads d_q as fma(0, gate, d_q) with gate = a result of the previous
@@ -311,34 +365,35 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
 #pragma unroll
           for (int cb = 0; cb < 2; ++cb) {
             const int p = 2 * j + ca, p2 = 2 * j2 + cb;
+#ifndef FO_HPART_SINGLE   // default: the four level blocks of an entry together
+            double e00, e01, e10, e11;
+            hpart4(ca, j, cb, j2, e00, e01, e10, e11);
+            if (p <= p2) {
+              sink.top(pk6(p, p2), e11);
+              sink.bot_add(p, p2, e00);
+            }
+            sink.off(p, p2, e01);
+            gate = e01;
+            if (j != j2) sink.off(p2, p, e10);
+#else
             if (p <= p2) {
               sink.top(pk6(p, p2), hpart(ca, j, 1, cb, j2, 1));
               sink.bot_add(p, p2, hpart(ca, j, 0, cb, j2, 0));
             }
-#ifndef FO_H_BT_IN_REGS
             const double v = hpart(ca, j, 0, cb, j2, 1);
             sink.off(p, p2, v);
             gate = v;
             if (j != j2) sink.off(p2, p, hpart(cb, j2, 0, ca, j, 1));
-#else
-            gate = sink.top_get(pk6(p <= p2 ? p : p2, p <= p2 ? p2 : p));
 #endif
           }
       }
   }
   if (w.go) {   // rank-1 (bottom, top), accumulated onto the frozen-viscosity part
     double acc[36];
-#ifndef FO_H_BT_IN_REGS
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
       for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
-#else   // the (bottom, top) frozen-viscosity part straight into the accumulators
-#pragma unroll
-    for (int p = 0; p < 6; ++p)
-#pragma unroll
-      for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = fma(0.0, gate, hpart(p & 1, p >> 1, 0, p2 & 1, p2 >> 1, 1));
-#endif
 FO_UNROLL(FO_UNROLL_R1A)
     for (int q = 0; q < 6; ++q) {   // rolled: not all six points' data live at once
       const int a = q >> 1;
@@ -347,15 +402,24 @@ FO_UNROLL(FO_UNROLL_R1A)
       const double f0 = 0.5 - 0.5 * zeta, f1 = 0.5 + 0.5 * zeta;
       const double dg = fma(0.0, gate, dq(q));
       double gb[6], gt[6];
+#ifdef FO_QSCALED
+      const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
+      (void)rho_a;
+#endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
+#ifdef FO_QSCALED
+        const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
+#else
         const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
+        const double qu = rj * Qu(q), qv = rj * Qv(q);
+#endif
         const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
         const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
-        gb[2 * j] = dg * fma(f0, pu, -rj * Qu(q));
-        gb[2 * j + 1] = dg * fma(f0, pv, -rj * Qv(q));
-        gt[2 * j] = fma(f1, pu, rj * Qu(q));
-        gt[2 * j + 1] = fma(f1, pv, rj * Qv(q));
+        gb[2 * j] = dg * fma(f0, pu, -qu);
+        gb[2 * j + 1] = dg * fma(f0, pv, -qv);
+        gt[2 * j] = fma(f1, pu, qu);
+        gt[2 * j + 1] = fma(f1, pv, qv);
       }
 #pragma unroll
       for (int p = 0; p < 6; ++p)
@@ -388,12 +452,20 @@ FO_UNROLL(FO_UNROLL_R1B)
       const double dd = fma(0.0, gate, dq(q));
       const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
       double gb[6], gt[6], dgb[6], dgt[6];
+#ifdef FO_QSCALED
+      const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
+      (void)rho_a;
+#endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
+#ifdef FO_QSCALED
+        const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
+#else
         const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
+        const double qu = rj * Qu(q), qv = rj * Qv(q);
+#endif
         const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
         const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
-        const double qu = rj * Qu(q), qv = rj * Qv(q);
         gb[2 * j] = fma(f0, pu, -qu);
         gb[2 * j + 1] = fma(f0, pv, -qv);
         gt[2 * j] = fma(f1, pu, qu);

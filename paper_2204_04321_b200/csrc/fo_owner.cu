@@ -380,6 +380,9 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     sp.nedge = __ldg(pv.nedge + p);
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
+  // the mbarrier is initialised before any warp can wait on it (warps without
+  // triangles reach the first bulk_wait at once)
+  __syncthreads();
 #ifdef FO_STAGGER_NS
   // experiment: the second CTA of each SM in the first wave starts late, so
   // the two resident CTAs alternate their element and gather phases
