@@ -140,7 +140,8 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   }
   // ---- quadrature loop: compact per-point data
   double cq[6];
-  // compact per point q: d, e1x, e1y = e2x = eps_xy, Qu, e2y, Qv (6 values)
+  // compact per point q: d, e1x, e1y = e2x = eps_xy, Qu, e2y, Qv (6 values; Qu, Qv
+  // stored as rho_a Q / 6, so that r_j Q = (j == a ? 4 : 1) x the stored value)
 #define dq(q) cmp(6 * (q) + 0)
 #define E1x(q) cmp(6 * (q) + 1)
 #define E1y(q) cmp(6 * (q) + 2)
@@ -170,7 +171,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         // strain-rate vectors
         const double e1x = 2.0 * ux + vy, e1y = exy, e1z = exz;
         const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
-#ifdef FO_QSCALED   // stored as rho_a Q / 6: r_j Q = (j == a ? 4 : 1) x the stored value
+#ifndef FO_Q_UNSCALED   // default: stored as rho_a Q / 6: r_j Q = (j == a ? 4 : 1) x the stored value
         const double r6 = rho[a] * kSixth;
         Qu(q) = (e1z - e1x * zx - e1y * zy) * r6;
         Qv(q) = (e2z - e2x * zx - e2y * zy) * r6;
@@ -402,13 +403,13 @@ FO_UNROLL(FO_UNROLL_R1A)
       const double f0 = 0.5 - 0.5 * zeta, f1 = 0.5 + 0.5 * zeta;
       const double dg = fma(0.0, gate, dq(q));
       double gb[6], gt[6];
-#ifdef FO_QSCALED
+#ifndef FO_Q_UNSCALED
       const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
       (void)rho_a;
 #endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-#ifdef FO_QSCALED
+#ifndef FO_Q_UNSCALED
         const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
 #else
         const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
@@ -452,13 +453,13 @@ FO_UNROLL(FO_UNROLL_R1B)
       const double dd = fma(0.0, gate, dq(q));
       const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
       double gb[6], gt[6], dgb[6], dgt[6];
-#ifdef FO_QSCALED
+#ifndef FO_Q_UNSCALED
       const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
       (void)rho_a;
 #endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-#ifdef FO_QSCALED
+#ifndef FO_Q_UNSCALED
         const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
 #else
         const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
