@@ -373,11 +373,9 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
               sink.top(pk6(p, p2), e11);
               sink.bot_add(p, p2, e00);
             }
+            sink.off(p, p2, e01);
             gate = e01;
-            if (!Sink::kPairedO) {   // paired O: the (bottom, top) part goes straight to the accumulators
-              sink.off(p, p2, e01);
-              if (j != j2) sink.off(p2, p, e10);
-            }
+            if (j != j2) sink.off(p2, p, e10);
 #else
             if (p <= p2) {
               sink.top(pk6(p, p2), hpart(ca, j, 1, cb, j2, 1));
@@ -393,21 +391,10 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
   }
   if (w.go) {   // rank-1 (bottom, top), accumulated onto the frozen-viscosity part
     double acc[36];
-    if (Sink::kPairedO) {
 #pragma unroll
-      for (int p = 0; p < 6; ++p)
+    for (int p = 0; p < 6; ++p)
 #pragma unroll
-        for (int p2 = 0; p2 < 6; ++p2) {   // entry (row p, column p2) = e01 of (p, p2)
-          double e00, e01, e10, e11;
-          hpart4(p & 1, p >> 1, p2 & 1, p2 >> 1, e00, e01, e10, e11);
-          acc[6 * p + p2] = fma(0.0, gate, e01);
-        }
-    } else {
-#pragma unroll
-      for (int p = 0; p < 6; ++p)
-#pragma unroll
-        for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
-    }
+      for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
 FO_UNROLL(FO_UNROLL_R1A)
     for (int q = 0; q < 6; ++q) {   // rolled: not all six points' data live at once
       const int a = q >> 1;
@@ -443,7 +430,7 @@ FO_UNROLL(FO_UNROLL_R1A)
 #pragma unroll
     for (int p = 0; p < 6; ++p)
 #pragma unroll
-      for (int p2 = 0; p2 < 6; p2 += 2) sink.off2(p, p2, acc[6 * p + p2], acc[6 * p + p2 + 1]);
+      for (int p2 = 0; p2 < 6; ++p2) sink.off(p, p2, acc[6 * p + p2]);
     gate = acc[35];
   }
   if (w.go) {   // rank-1 (bottom, bottom) and (top, top) in one pass, with both

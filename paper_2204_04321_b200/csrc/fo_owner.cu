@@ -80,15 +80,6 @@ constexpr int kD = 27;   // level-k diagonal block (21, 2x2-block layout) + 6 re
 constexpr int kO = 36;   // 6x6 bottom-top block of wedge k
 constexpr int kC = 36;   // compact per-point scratch (6 x 6 quadrature points)
 constexpr int kSlotsPerTri = kD + kO + kC;
-// O (bottom, top) entry i = 6p + p2 of triangle slot tl.  FO_O_PAIRED: entries
-// 2m, 2m + 1 of a triangle form one 16-byte double2 ([i/2][tl]), so phase B
-// reads a row's two column components with one LDS.128 (O first in shared
-// memory: 16-byte aligned)
-#ifdef FO_O_PAIRED
-__device__ __forceinline__ constexpr int oidx(int i, int tl) { return (i >> 1) * 2 * TP + 2 * tl + (i & 1); }
-#else
-__device__ __forceinline__ constexpr int oidx(int i, int tl) { return i * TP + tl; }
-#endif
 // byte offset of the plan in dynamic shared memory (16-byte aligned for the bulk copy)
 constexpr int kPlanOffset = (kSlotsPerTri * TP * 8 + 15) / 16 * 16;
 // residual only (KR): the residual slots of D (6) and the compact scratch, so
@@ -171,29 +162,6 @@ __device__ __forceinline__ void gather2(uint2 c2, const double* D, const double*
     s.dg[3] = (s.dg[3] + Da[saa + sba]) + Db[sab + sbb];
   }
   if (UP) {
-#ifdef FO_O_PAIRED
-    const double2* O2 = reinterpret_cast<const double2*>(O);
-    const double2* Oua = O2 + (int((c2.x >> 15) & 31) >> 1) * TP + tla;
-    const double2* Ona = O2 + (int((c2.x >> 20) & 31) >> 1) * TP + tla;
-    const double2* Oub = O2 + (int((c2.y >> 15) & 31) >> 1) * TP + tlb;
-    const double2* Onb = O2 + (int((c2.y >> 20) & 31) >> 1) * TP + tlb;
-    // rows p, p + 1 of the block are 3 pairs apart: up = (row p: b 0,1), (row p+1:
-    // b 0,1); nx (transposed) = (Ona[0].x, Ona[3].x, Ona[0].y, Ona[3].y)
-    const double2 ua0 = Oua[0], ua1 = Oua[3 * TP], ub0 = Oub[0], ub1 = Oub[3 * TP];
-    const double2 na0 = Ona[0], na1 = Ona[3 * TP], nb0 = Onb[0], nb1 = Onb[3 * TP];
-    const double uva[4] = {ua0.x, ua0.y, ua1.x, ua1.y}, uvb[4] = {ub0.x, ub0.y, ub1.x, ub1.y};
-    const double nva[4] = {na0.x, na1.x, na0.y, na1.y}, nvb[4] = {nb0.x, nb1.x, nb0.y, nb1.y};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (FIRST) {
-        s.up[i] = uva[i] + uvb[i];
-        s.nx[i] = nva[i] + nvb[i];
-      } else {
-        s.up[i] = (s.up[i] + uva[i]) + uvb[i];
-        s.nx[i] = (s.nx[i] + nva[i]) + nvb[i];
-      }
-    }
-#else
     const double* Oua = O + int((c2.x >> 15) & 31) * TP + tla;
     const double* Ona = O + int((c2.x >> 20) & 31) * TP + tla;
     const double* Oub = O + int((c2.y >> 15) & 31) * TP + tlb;
@@ -209,7 +177,6 @@ __device__ __forceinline__ void gather2(uint2 c2, const double* D, const double*
         s.nx[i] = (s.nx[i] + Ona[on[i]]) + Onb[on[i]];
       }
     }
-#endif
   }
 }
 
@@ -325,19 +292,9 @@ struct PatchSink {
   double held[27];   // dmap layout
   __device__ __forceinline__ void r_bot_add(int p, double v) { D[(21 + p) * TP + tl] += v; }
   __device__ __forceinline__ void bot_add(int p, int p2, double v) { D[dmap(p, p2) * TP + tl] += v; }
-  __device__ __forceinline__ void off(int p, int p2, double v) { O[oidx(6 * p + p2, tl)] = v; }
-  __device__ __forceinline__ void off_add(int p, int p2, double v) { O[oidx(6 * p + p2, tl)] += v; }
-  __device__ __forceinline__ double off_get(int p, int p2) const { return O[oidx(6 * p + p2, tl)]; }
-#ifdef FO_O_PAIRED
-  static constexpr bool kPairedO = true;
-  // entries (p, p2), (p, p2 + 1), p2 even, as one 16-byte access
-  __device__ __forceinline__ void off2(int p, int p2, double v0, double v1) {
-    *reinterpret_cast<double2*>(O + oidx(6 * p + p2, tl)) = make_double2(v0, v1);
-  }
-#else
-  static constexpr bool kPairedO = false;
-  __device__ __forceinline__ void off2(int p, int p2, double v0, double v1) { off(p, p2, v0); off(p, p2 + 1, v1); }
-#endif
+  __device__ __forceinline__ void off(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] = v; }
+  __device__ __forceinline__ void off_add(int p, int p2, double v) { O[(6 * p + p2) * TP + tl] += v; }
+  __device__ __forceinline__ double off_get(int p, int p2) const { return O[(6 * p + p2) * TP + tl]; }
   __device__ __forceinline__ double bot_get(int p, int p2) const { return D[dmap(p, p2) * TP + tl]; }
   __device__ __forceinline__ void bot_set(int p, int p2, double v) { D[dmap(p, p2) * TP + tl] = v; }
   __device__ __forceinline__ double top_get(int i) const {
@@ -371,11 +328,9 @@ struct PatchSink {
 // residual-only sink: the Jacobian parts of the element are dead code; D is
 // the compact KR layout (the 6 residual slots only)
 struct PatchSinkR {
-  static constexpr bool kPairedO = false;
   double* D;
   int tl;
   double held[27];
-  __device__ __forceinline__ void off2(int, int, double, double) {}
   __device__ __forceinline__ void r_bot_add(int p, double v) { D[p * TP + tl] += v; }
   __device__ __forceinline__ void bot_add(int, int, double) {}
   __device__ __forceinline__ void off(int, int, double) {}
@@ -404,13 +359,8 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
                 PlanView pv, const double* __restrict__ U, double* __restrict__ R,
                 double* __restrict__ vals) {
   extern __shared__ __align__(16) double smem[];
-#ifdef FO_O_PAIRED
-  double* const O = smem;                                       // [kO/2][TP] double2
-  double* const D = NEED_J ? smem + kO * TP : smem;             // [kD][TP] (KR: [kDR][TP])
-#else
   double* const D = smem;                                       // [kD][TP] (KR: [kDR][TP])
   double* const O = smem + kD * TP;                             // [kO][TP] (KR: unused)
-#endif
   double* const C = smem + (NEED_J ? kD + kO : kDR) * TP;       // [kC][TP]
   const int p = blockIdx.x;
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
@@ -460,7 +410,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   }
   // triangle slot kPatchTris: the zero column the plan's pad entries read
   if (threadIdx.x < (NEED_J ? kD : kDR)) D[threadIdx.x * TP + kPatchTris] = 0.0;
-  if (NEED_J && threadIdx.x < kO) O[oidx(threadIdx.x, kPatchTris)] = 0.0;
+  if (NEED_J && threadIdx.x < kO) O[threadIdx.x * TP + kPatchTris] = 0.0;
   for (int k = 0; k < L; ++k) {
     typename std::conditional<NEED_J, PatchSink, PatchSinkR>::type sk;
     sk.D = D;
