@@ -137,6 +137,46 @@ def ncu_summary(config_name):
     return d if d.get("config") == config_name else None
 
 
+def roofline_entry(alg_bytes, kernel_ms, kernel_ms_total, step_ms_total, n_elems, peak_gbs, peak_src, prof,
+                   kernel_name):
+    """the bench line's `roofline` object for the dominant kernel: HBM fraction
+    of the algorithmic bytes per launch, FP64 fraction of the ncu-counted flops
+    (committed capture `prof`, may be None), and the binding roof.  When the
+    binding roof is FP64 (plain fp64 ALU arithmetic, no tensor cores: DESIGN.md
+    section 7) the object reports "bound": "alu" against the derived FP64 peak
+    and keeps the metric's HBM fraction under "hbm"."""
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s", "frac": achieved / peak_gbs,
+            "traffic": prof.get("dram_bytes_per_launch") if prof else None, "kernel": kernel_name,
+            "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms_total / max(step_ms_total, 1e-12),
+            "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+            "bytes_formula": "8 nnz + 32 N_nodes + 40 N_cols + 12 N_tri (SURVEY.md 8(d) d3)"}
+    fpw = prof.get("fp64_flop_per_wedge") if prof else None
+    if fpw:
+        tfl = fpw * n_elems / (kernel_ms / 1e3) / 1e12
+        fp64 = {"achieved": tfl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": tfl / FP64_PEAK_TFLOPS,
+                "flop_per_wedge": fpw, "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz",
+                "flop_source": prof.get("source")}
+        binding = "fp64" if fp64["frac"] > roof["frac"] else "hbm"
+        roof["min_roof"] = {"binding": binding, "frac": max(fp64["frac"], roof["frac"])}
+        if binding == "fp64":
+            hbm = {k: roof.pop(k) for k in ("achieved", "peak", "unit", "frac", "peak_source", "bytes_formula",
+                                            "algorithmic_bytes_per_launch")}
+            roof.pop("bound")
+            roof = {"bound": "alu", "achieved": fp64["achieved"], "peak": fp64["peak"], "unit": "TFLOP/s",
+                    "frac": fp64["frac"], "traffic": roof.pop("traffic"), **roof,
+                    "flop_per_wedge": fpw, "peak_source": fp64["peak_source"],
+                    "flop_source": fp64["flop_source"], "hbm": hbm}
+        else:
+            roof["fp64"] = fp64
+    if prof:
+        roof["ncu"] = {k: prof.get(k) for k in ("fp64_pipe_pct", "registers_per_thread", "warps_active_pct",
+                                                 "l1_data_pipe_pct", "shared_wavefronts", "shared_bank_conflicts",
+                                                 "l2_red_sectors_per_s") if prof.get(k) is not None}
+        roof["ncu"]["spills"] = 0   # ptxas -v of the build (DESIGN.md section 7)
+    return roof
+
+
 def _host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -329,45 +369,9 @@ def main():
     has_A = fp.A_elem is not None
     alg = algorithmic_bytes(mesh.n_elems, graph.nnz, mesh.n_nodes, n_cols, n_tri_local, has_A)
     kavg = kern_ms / max(kern_n, 1)
-    achieved = alg / (kavg / 1e3) / 1e9
     prof = ncu_summary(cfg_name)
-    traffic = None
-    fp64 = None
-    if prof:
-        traffic = prof.get("dram_bytes_per_launch")
-        fpw = prof.get("fp64_flop_per_wedge")
-        if fpw:
-            tfl = fpw * mesh.n_elems / (kavg / 1e3) / 1e12
-            fp64 = {"achieved": tfl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": tfl / FP64_PEAK_TFLOPS,
-                    "flop_per_wedge": fpw, "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz",
-                    "flop_source": prof.get("source")}
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "ka_patch_kernel" if args.scatter == 0 else "assemble_atomic_kernel",
-            "kernel_ms": kavg, "kernel_share_of_step": kern_ms / max(sum(step_ms), 1e-12),
-            "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
-            "bytes_formula": "8 nnz + 32 N_nodes + 40 N_cols + 12 N_tri (SURVEY.md 8(d) d3)"}
-    if fp64:
-        # the binding roof is the larger floor.  When it is
-        # the FP64 pipe (plain fp64 ALU arithmetic, no tensor cores: DESIGN.md
-        # section 7), the line reports "bound": "alu" against the derived FP64
-        # peak and keeps the metric's HBM fraction under "hbm".
-        binding = "fp64" if fp64["frac"] > roof["frac"] else "hbm"
-        roof["min_roof"] = {"binding": binding, "frac": max(fp64["frac"], roof["frac"])}
-        if binding == "fp64":
-            hbm = {k: roof.pop(k) for k in ("achieved", "peak", "unit", "frac", "peak_source", "bytes_formula",
-                                            "algorithmic_bytes_per_launch")}
-            roof.pop("bound")
-            roof = {"bound": "alu", "achieved": fp64["achieved"], "peak": fp64["peak"], "unit": "TFLOP/s",
-                    "frac": fp64["frac"], "traffic": roof.pop("traffic"), **roof,
-                    "flop_per_wedge": fp64["flop_per_wedge"], "peak_source": fp64["peak_source"],
-                    "flop_source": fp64["flop_source"], "hbm": hbm}
-        else:
-            roof["fp64"] = fp64
-    if prof:
-        roof["ncu"] = {k: prof.get(k) for k in ("fp64_pipe_pct", "registers_per_thread", "warps_active_pct",
-                                                 "l1_data_pipe_pct", "shared_wavefronts", "shared_bank_conflicts",
-                                                 "l2_red_sectors_per_s") if prof.get(k) is not None}
-        roof["ncu"]["spills"] = 0   # ptxas -v of the build
+    roof = roofline_entry(alg, kavg, kern_ms, sum(step_ms), mesh.n_elems, peak, peak_src, prof,
+                          "ka_patch_kernel" if args.scatter == 0 else "assemble_atomic_kernel")
 
     # residual only (KR), the same timing protocol
     r_ms = []
