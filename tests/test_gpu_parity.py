@@ -318,7 +318,7 @@ def test_host_buffer_entry_point(torch_cuda):
 def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
     """C3 (and C5, with its floating shelves) at full size in the bench's launch
     configuration: complete rows of sampled columns vs the oracle on the
-    sub-footprint of their triangle fans."""
+    sub-footprint of their triangle fans (R + J kernel and residual-only kernel)."""
     import torch
     from paper_2204_04321_b200 import fo
     fp = mg.greenland_like_1_10() if cfg == "C3" else mg.antarctica_like()
@@ -326,8 +326,10 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
     U = torch.tensor(fp.U, device="cuda")
     g = mesh.graph()
     R, vals = mesh.jacobian(U)
+    Rr = mesh.residual(U)   # the residual-only kernel (KR, compact shared layout)
     torch.cuda.synchronize()
     R = R.cpu().numpy()
+    Rr = Rr.cpu().numpy()
     rp = np.empty(g.n_rows + 1, np.int64)
     rp, _ = g.to_host()
     vals = vals.cpu().numpy()
@@ -348,6 +350,7 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
                 r_g = 2 * (c * L1 + k) + a
                 r_o = 2 * (lc * L1 + k) + a
                 assert abs(R[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
+                assert abs(Rr[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
                 seg_g = vals[rp[r_g]:rp[r_g + 1]]
                 seg_o = ov[orp[r_o]:orp[r_o + 1]]
                 assert seg_g.size == seg_o.size
