@@ -314,15 +314,19 @@ def test_host_buffer_entry_point(torch_cuda):
     assert np.abs(Vh.numpy() - Vd.cpu().numpy()).max() <= 1e-13 * np.abs(Vh.numpy()).max()
 
 
-@pytest.mark.parametrize("cfg", ["C3", "C5"])
+@pytest.mark.parametrize("cfg", ["C3", "C5", "C3-tet"])
 def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
     """C3 (and C5, with its floating shelves) at full size in the bench's launch
     configuration: complete rows of sampled columns vs the oracle on the
     sub-footprint of their triangle fans (R + J kernel and residual-only kernel)."""
     import torch
     from paper_2204_04321_b200 import fo
-    fp = mg.greenland_like_1_10() if cfg == "C3" else mg.antarctica_like()
+    fp = mg.antarctica_like() if cfg == "C5" else mg.greenland_like_1_10()
+    if cfg == "C3-tet":   # NEXT-f4 at full size: three tetrahedra per prism
+        fp.elem_type = 1
     mesh = fo.Mesh.from_footprint(fp)
+    if cfg == "C3-tet":
+        mesh.set_element(1)
     U = torch.tensor(fp.U, device="cuda")
     g = mesh.graph()
     R, vals = mesh.jacobian(U)
