@@ -22,14 +22,19 @@
  * Readings where the paper is silent (quadrature, regularisation, basal measure,
  * floating mask, numbering) are listed in DESIGN.md section "Readings".
  *
- * Pins (tests/test_oracle_pins.py, tests/test_oracle_pins_next.py; SURVEY.md
- * 8(c) c4): closed-form P1 right-prism operators (n = 1), affinity, the patch
- * test, driving-stress and basal totals, partition of unity, Glen homogeneity,
+ * Pins (tests/test_oracle_pins.py, tests/test_oracle_pins_next.py,
+ * tests/test_oracle_pins_pernode.py): closed-form P1
+ * right-prism operators (n = 1), affinity, the patch test, driving-stress and
+ * basal totals AND their per-node closed forms (int phi_i on columns of unequal
+ * height; beta = hat function of one vertex) for wedges, tets and hexes --
+ * tools/mutate_oracle.py shows a rotation of either term's node weights fails
+ * them --, partition of unity, Glen homogeneity,
  * Euler identities, the rigid nullspace, symmetry and convexity, FD Jacobian and
  * FD energy gradient, brute-force graph counts, the paper's mesh sizes
  * (tests/golden/paper_counts.json); NEXT rows: the floating-front integral, level
  * split, Q = 0 and temperature-ratio laws, tet / hex patch tests and closed forms.
- * Parity unpinned: no function is unpinned as a whole, but PAPER.md prints no
+ * Parity unpinned: no function is unpinned (DESIGN.md section 3 names the pin
+ * of every function and term), but PAPER.md prints no
  * residual or Jacobian value, so ABSOLUTE values at C2-C5 rest on these pins and
  * on the conventions L4, L7-L10 the paper leaves open.
  *
