@@ -261,6 +261,20 @@ FO_API fo_status fo_kernel_time_ms(fo_mesh m, double* total_ms, int32_t* n_launc
 FO_API fo_status fo_nccl_unique_id(void* id128);
 FO_API fo_status fo_halo_create(fo_mesh local, fo_graph local_g, const void* nccl_unique_id,
                          int32_t rank, int32_t n_ranks, fo_halo* out);
+/* Loopback transport (one process, one device): creates the n_parts halos of
+ * one partition at once, out[p] for parts[p] (the local mesh of part p, made
+ * with fo_mesh_create_part, and its graph).  fo_halo_import / fo_halo_sum on
+ * these halos run the same plans, staging buffers, gather and unpack-add
+ * kernels and sender order as the NCCL halos; only the point-to-point
+ * transfers are device-to-device copies on the callers' streams instead of
+ * ncclSend / ncclRecv.  Sends are eager; a part's unpack-add is enqueued when
+ * the last slice it receives has been sent, which can be inside a later part's
+ * call -- so call a phase (import, sum) for every part before enqueueing work
+ * that depends on it.  Used to run the halo path on one GPU (tests, bench).
+ * Errors: FO_EINVAL (NULL, different devices), FO_ESTATE (parts[p] is not part
+ * p of one n_parts partition of one footprint, or graph/mesh mismatch). */
+FO_API fo_status fo_halo_create_loopback(const fo_mesh* parts, const fo_graph* graphs, int32_t n_parts,
+                                         fo_halo* out);
 /* ghost U <- owners' U (owned prefix of d_U is read, ghost part written) */
 FO_API fo_status fo_halo_import(fo_halo h, double* d_U, void* stream);
 /* owners' rows += ghost-row partial sums of the other ranks; after the call

@@ -14,6 +14,11 @@
 
 #include <algorithm>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -133,10 +138,41 @@ fo_status dev_copy(T** dst, const std::vector<T>& v) {
 }  // namespace
 }  // namespace fo
 
+namespace fo {
+// Loopback transport: the P parts of a partitioned mesh held by ONE process
+// (one device), for running the halo code path without a second GPU.  It
+// stands in for NCCL's point-to-point calls only -- the plans, staging
+// buffers, gather / unpack-add kernels and the sender order of fo_halo_import
+// and fo_halo_sum are the same code.  A send is eager (copied into a
+// stream-ordered scratch buffer on the sender's stream, an event recorded); a
+// recv is completed, on the receiver's stream after that event, as soon as
+// the matching send exists (the k-th send p -> q matches the k-th recv of q
+// from p, NCCL's ordering).  Work that depends on a recv (the unpack-add) is
+// enqueued when the last recv of its group completes, which may happen inside
+// a later part's call: every part must enter a phase (import, sum) before
+// work that depends on it is enqueued on any part.
+struct LoopOp {                 // one group of a halo call
+  int pending = 0;
+  bool ended = false;
+  std::function<fo_status()> cont;   // enqueued when all recvs completed
+};
+struct LoopSend { double* buf; int64_t n; cudaEvent_t ev; };
+struct LoopRecv { double* dst; int64_t n; cudaStream_t s; std::shared_ptr<LoopOp> op; };
+struct LoopGroup {
+  std::mutex mu;
+  int device = 0;
+  std::map<std::pair<int32_t, int32_t>, std::deque<LoopSend>> sends;   // (from, to)
+  std::map<std::pair<int32_t, int32_t>, std::deque<LoopRecv>> recvs;
+  fo_status error = FO_OK;
+};
+}  // namespace fo
+
 struct fo_halo_s {
   int device = 0;
   int32_t rank = 0, n_ranks = 1, L = 0;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<fo::LoopGroup> loop;    // loopback transport, else NCCL
+  std::shared_ptr<fo::LoopOp> op;         // the loopback group being posted
   // owners q of my ghost columns: sum sends my slices to q, import receives
   // q's U into my ghost slice [row0, row0 + nrows)
   struct Owner { int32_t q; int64_t row0, nrows, val0, nvals; };
@@ -151,6 +187,93 @@ struct fo_halo_s {
   std::vector<Owner> owners;
   std::vector<Holder> holders;
 };
+
+namespace fo {
+namespace {
+
+// ---- point-to-point transport: NCCL, or the loopback group ----
+fo_status loop_match(LoopGroup& G, std::pair<int32_t, int32_t> ch) {
+  auto& S = G.sends[ch];
+  auto& Rq = G.recvs[ch];
+  while (!S.empty() && !Rq.empty()) {
+    LoopSend sd = S.front();
+    LoopRecv rv = Rq.front();
+    S.pop_front();
+    Rq.pop_front();
+    if (sd.n != rv.n) return fail(FO_ESTATE, "loopback: send / recv sizes differ");
+    fo_status st = cuda_status(cudaStreamWaitEvent(rv.s, sd.ev, 0), "cudaStreamWaitEvent");
+    if (!st) st = cuda_status(cudaMemcpyAsync(rv.dst, sd.buf, sizeof(double) * size_t(sd.n),
+                                              cudaMemcpyDeviceToDevice, rv.s), "cudaMemcpyAsync");
+    if (!st) st = cuda_status(cudaFreeAsync(sd.buf, rv.s), "cudaFreeAsync");
+    cudaEventDestroy(sd.ev);
+    if (st) return st;
+    if (--rv.op->pending == 0 && rv.op->ended && rv.op->cont) {
+      st = rv.op->cont();
+      rv.op->cont = nullptr;
+      if (st) return st;
+    }
+  }
+  return FO_OK;
+}
+
+fo_status xp_group_start(fo_halo h) {
+  if (h->loop) {
+    h->op = std::make_shared<LoopOp>();
+    return FO_OK;
+  }
+  return nccl_status(ncclGroupStart(), "ncclGroupStart");
+}
+
+fo_status xp_send(fo_halo h, const double* buf, int64_t n, int32_t peer, cudaStream_t s) {
+  if (!h->loop) return nccl_status(ncclSend(buf, size_t(n), ncclDouble, peer, h->comm, s), "ncclSend");
+  LoopGroup& G = *h->loop;
+  std::lock_guard<std::mutex> lk(G.mu);
+  LoopSend sd{nullptr, n, nullptr};
+  fo_status st = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&sd.buf),
+                                             sizeof(double) * size_t(std::max<int64_t>(n, 1)), s),
+                             "cudaMallocAsync");
+  if (!st && n > 0)
+    st = cuda_status(cudaMemcpyAsync(sd.buf, buf, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, s),
+                     "cudaMemcpyAsync");
+  if (!st) st = cuda_status(cudaEventCreateWithFlags(&sd.ev, cudaEventDisableTiming), "cudaEventCreate");
+  if (!st) st = cuda_status(cudaEventRecord(sd.ev, s), "cudaEventRecord");
+  if (st) return st;
+  const auto ch = std::make_pair(h->rank, peer);
+  G.sends[ch].push_back(sd);
+  return loop_match(G, ch);
+}
+
+fo_status xp_recv(fo_halo h, double* buf, int64_t n, int32_t peer, cudaStream_t s) {
+  if (!h->loop) return nccl_status(ncclRecv(buf, size_t(n), ncclDouble, peer, h->comm, s), "ncclRecv");
+  LoopGroup& G = *h->loop;
+  std::lock_guard<std::mutex> lk(G.mu);
+  ++h->op->pending;
+  const auto ch = std::make_pair(peer, h->rank);
+  G.recvs[ch].push_back({buf, n, s, h->op});
+  return loop_match(G, ch);
+}
+
+// ends the group; `cont` (the work that consumes the received data) is
+// enqueued now (NCCL: stream order covers the recvs) or, on the loopback,
+// when the group's last recv completes
+fo_status xp_group_end(fo_halo h, std::function<fo_status()> cont) {
+  if (!h->loop) {
+    fo_status st = nccl_status(ncclGroupEnd(), "ncclGroupEnd");
+    if (st) return st;
+    return cont ? cont() : FO_OK;
+  }
+  LoopGroup& G = *h->loop;
+  std::lock_guard<std::mutex> lk(G.mu);
+  auto op = h->op;
+  h->op.reset();
+  op->ended = true;
+  if (op->pending == 0) return cont ? cont() : FO_OK;
+  op->cont = std::move(cont);
+  return FO_OK;
+}
+
+}  // namespace
+}  // namespace fo
 
 using namespace fo;
 
@@ -236,6 +359,49 @@ fo_status fo_nccl_unique_id(void* id128) {
   return st;
 }
 
+}  // extern "C"
+
+namespace fo {
+namespace {
+// the plan of one rank (owners / holders, device maps and staging), shared by
+// the NCCL and the loopback transports
+fo_status halo_plan(fo_halo h, fo_mesh local) {
+  const int64_t nv = local->global_n_vert, nt = int64_t(local->global_tri.size() / 3);
+  const int32_t* gtri = local->global_tri.data();
+  const int32_t* part = local->global_part.data();
+  const int32_t n_ranks = h->n_ranks, rank = h->rank;
+  const auto own = owners(nv, nt, gtri, part);
+  std::vector<Topo> T(static_cast<size_t>(n_ranks));
+  fo_status st = FO_OK;
+  for (int32_t p = 0; p < n_ranks && !st; ++p) st = build_topology(nv, nt, gtri, h->L, part, p, T[size_t(p)]);
+  if (st) return st;
+  std::vector<std::vector<int64_t>> loc(static_cast<size_t>(n_ranks));
+  for (int32_t p = 0; p < n_ranks; ++p) loc[size_t(p)] = local_index(T[size_t(p)], nv);
+  for (int32_t q = 0; q < n_ranks; ++q) {
+    if (q == rank) continue;
+    SendSlice S = plan_sends(T[size_t(rank)], T[size_t(q)], loc[size_t(q)], own, q, h->L);
+    if (S.nrows > 0) h->owners.push_back({q, S.row0, S.nrows, S.val0, S.nvals});
+  }
+  for (int32_t p = 0; p < n_ranks && !st; ++p) {
+    if (p == rank) continue;
+    SendSlice S = plan_sends(T[size_t(p)], T[size_t(rank)], loc[size_t(rank)], own, rank, h->L);
+    if (S.nrows == 0) continue;
+    fo_halo_s::Holder hd{p, S.nrows, S.nvals, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    st = dev_copy(&hd.d_rows, S.dest_rows);
+    if (!st) st = dev_copy(&hd.d_vals, S.dest_vals);
+    if (!st) st = dev_copy(&hd.d_imp_idx, S.import_src);
+    if (!st) st = cuda_status(cudaMalloc(&hd.d_buf_r, sizeof(double) * S.nrows), "cudaMalloc");
+    if (!st) st = cuda_status(cudaMalloc(&hd.d_imp_buf, sizeof(double) * S.nrows), "cudaMalloc");
+    if (!st) st = cuda_status(cudaMalloc(&hd.d_buf_v, sizeof(double) * std::max<int64_t>(1, S.nvals)), "cudaMalloc");
+    h->holders.push_back(hd);
+  }
+  return st;
+}
+}  // namespace
+}  // namespace fo
+
+extern "C" {
+
 fo_status fo_halo_create(fo_mesh local, fo_graph local_g, const void* nccl_unique_id, int32_t rank,
                          int32_t n_ranks, fo_halo* out) {
   if (!local || !local_g || !nccl_unique_id || !out) return fail(FO_EINVAL, "NULL argument");
@@ -253,33 +419,7 @@ fo_status fo_halo_create(fo_mesh local, fo_graph local_g, const void* nccl_uniqu
   h->n_ranks = n_ranks;
   h->L = local->L;
   if (n_ranks > 1) {
-    const int64_t nv = local->global_n_vert, nt = int64_t(local->global_tri.size() / 3);
-    const int32_t* gtri = local->global_tri.data();
-    const int32_t* part = local->global_part.data();
-    const auto own = owners(nv, nt, gtri, part);
-    std::vector<Topo> T(static_cast<size_t>(n_ranks));
-    for (int32_t p = 0; p < n_ranks && !st; ++p) st = build_topology(nv, nt, gtri, h->L, part, p, T[size_t(p)]);
-    if (st) { delete h; return st; }
-    std::vector<std::vector<int64_t>> loc(static_cast<size_t>(n_ranks));
-    for (int32_t p = 0; p < n_ranks; ++p) loc[size_t(p)] = local_index(T[size_t(p)], nv);
-    for (int32_t q = 0; q < n_ranks && !st; ++q) {
-      if (q == rank) continue;
-      SendSlice S = plan_sends(T[size_t(rank)], T[size_t(q)], loc[size_t(q)], own, q, h->L);
-      if (S.nrows > 0) h->owners.push_back({q, S.row0, S.nrows, S.val0, S.nvals});
-    }
-    for (int32_t p = 0; p < n_ranks && !st; ++p) {
-      if (p == rank) continue;
-      SendSlice S = plan_sends(T[size_t(p)], T[size_t(rank)], loc[size_t(rank)], own, rank, h->L);
-      if (S.nrows == 0) continue;
-      fo_halo_s::Holder hd{p, S.nrows, S.nvals, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-      st = dev_copy(&hd.d_rows, S.dest_rows);
-      if (!st) st = dev_copy(&hd.d_vals, S.dest_vals);
-      if (!st) st = dev_copy(&hd.d_imp_idx, S.import_src);
-      if (!st) st = cuda_status(cudaMalloc(&hd.d_buf_r, sizeof(double) * S.nrows), "cudaMalloc");
-      if (!st) st = cuda_status(cudaMalloc(&hd.d_imp_buf, sizeof(double) * S.nrows), "cudaMalloc");
-      if (!st) st = cuda_status(cudaMalloc(&hd.d_buf_v, sizeof(double) * std::max<int64_t>(1, S.nvals)), "cudaMalloc");
-      h->holders.push_back(hd);
-    }
+    st = halo_plan(h, local);
     if (!st) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_unique_id, sizeof(id));
@@ -291,9 +431,43 @@ fo_status fo_halo_create(fo_mesh local, fo_graph local_g, const void* nccl_uniqu
   return FO_OK;
 }
 
+fo_status fo_halo_create_loopback(const fo_mesh* parts, const fo_graph* graphs, int32_t n_parts,
+                                  fo_halo* out) {
+  if (!parts || !graphs || !out || n_parts < 1) return fail(FO_EINVAL, "NULL argument or n_parts < 1");
+  for (int32_t p = 0; p < n_parts; ++p) out[p] = nullptr;
+  for (int32_t p = 0; p < n_parts; ++p) {
+    if (!parts[p] || !graphs[p]) return fail(FO_EINVAL, "NULL mesh or graph");
+    if (graphs[p]->mesh != parts[p]) return fail(FO_ESTATE, "graph was built for another mesh");
+    if (parts[p]->n_parts != n_parts || parts[p]->part != p)
+      return fail(FO_ESTATE, "parts[p] must be the local mesh of part p of an n_parts partition");
+    if (parts[p]->device != parts[0]->device) return fail(FO_EINVAL, "loopback parts must share one device");
+    if (n_parts > 1 && (parts[p]->global_tri != parts[0]->global_tri ||
+                        parts[p]->global_part != parts[0]->global_part))
+      return fail(FO_ESTATE, "parts come from different footprints or partitions");
+  }
+  fo_status st = cuda_status(cudaSetDevice(parts[0]->device), "cudaSetDevice");
+  if (st) return st;
+  auto G = std::make_shared<LoopGroup>();
+  G->device = parts[0]->device;
+  for (int32_t p = 0; p < n_parts && !st; ++p) {
+    fo_halo h = new fo_halo_s();
+    h->device = parts[p]->device;
+    h->rank = p;
+    h->n_ranks = n_parts;
+    h->L = parts[p]->L;
+    h->loop = G;
+    out[p] = h;
+    if (n_parts > 1) st = halo_plan(h, parts[p]);
+  }
+  if (st)
+    for (int32_t p = 0; p < n_parts; ++p) { fo_halo_destroy(out[p]); out[p] = nullptr; }
+  return st;
+}
+
 fo_status fo_halo_import(fo_halo h, double* d_U, void* stream) {
   if (!h) return fail(FO_EINVAL, "halo is NULL");
   if (h->n_ranks == 1) return FO_OK;
+  if (!d_U) return fail(FO_EINVAL, "d_U is NULL");
   fo_status st = cuda_status(cudaSetDevice(h->device), "cudaSetDevice");
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -301,12 +475,12 @@ fo_status fo_halo_import(fo_halo h, double* d_U, void* stream) {
     gather_kernel<<<grid_for(hd.nrows), 256, 0, s>>>(d_U, hd.d_imp_idx, hd.d_imp_buf, hd.nrows);
   st = cuda_status(cudaGetLastError(), "gather_kernel");
   if (st) return st;
-  st = nccl_status(ncclGroupStart(), "ncclGroupStart");
+  st = xp_group_start(h);
   for (auto& hd : h->holders)
-    if (!st) st = nccl_status(ncclSend(hd.d_imp_buf, size_t(hd.nrows), ncclDouble, hd.p, h->comm, s), "ncclSend");
+    if (!st) st = xp_send(h, hd.d_imp_buf, hd.nrows, hd.p, s);
   for (auto& o : h->owners)
-    if (!st) st = nccl_status(ncclRecv(d_U + o.row0, size_t(o.nrows), ncclDouble, o.q, h->comm, s), "ncclRecv");
-  fo_status st2 = nccl_status(ncclGroupEnd(), "ncclGroupEnd");
+    if (!st) st = xp_recv(h, d_U + o.row0, o.nrows, o.q, s);
+  fo_status st2 = xp_group_end(h, nullptr);
   return st ? st : st2;
 }
 
@@ -316,28 +490,27 @@ fo_status fo_halo_sum(fo_halo h, double* d_R, double* d_vals, void* stream) {
   fo_status st = cuda_status(cudaSetDevice(h->device), "cudaSetDevice");
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = nccl_status(ncclGroupStart(), "ncclGroupStart");
+  st = xp_group_start(h);
   for (auto& o : h->owners) {
     if (st) break;
-    if (d_R) st = nccl_status(ncclSend(d_R + o.row0, size_t(o.nrows), ncclDouble, o.q, h->comm, s), "ncclSend");
-    if (!st && d_vals && o.nvals > 0)
-      st = nccl_status(ncclSend(d_vals + o.val0, size_t(o.nvals), ncclDouble, o.q, h->comm, s), "ncclSend");
+    if (d_R) st = xp_send(h, d_R + o.row0, o.nrows, o.q, s);
+    if (!st && d_vals && o.nvals > 0) st = xp_send(h, d_vals + o.val0, o.nvals, o.q, s);
   }
   for (auto& hd : h->holders) {
     if (st) break;
-    if (d_R) st = nccl_status(ncclRecv(hd.d_buf_r, size_t(hd.nrows), ncclDouble, hd.p, h->comm, s), "ncclRecv");
-    if (!st && d_vals && hd.nvals > 0)
-      st = nccl_status(ncclRecv(hd.d_buf_v, size_t(hd.nvals), ncclDouble, hd.p, h->comm, s), "ncclRecv");
+    if (d_R) st = xp_recv(h, hd.d_buf_r, hd.nrows, hd.p, s);
+    if (!st && d_vals && hd.nvals > 0) st = xp_recv(h, hd.d_buf_v, hd.nvals, hd.p, s);
   }
-  fo_status st2 = nccl_status(ncclGroupEnd(), "ncclGroupEnd");
-  if (st || st2) return st ? st : st2;
-  // deterministic unpack: senders in ascending rank order
-  for (auto& hd : h->holders) {
-    if (d_R) scatter_add_kernel<<<grid_for(hd.nrows), 256, 0, s>>>(hd.d_buf_r, hd.d_rows, d_R, hd.nrows);
-    if (d_vals && hd.nvals > 0)
-      scatter_add_kernel<<<grid_for(hd.nvals), 256, 0, s>>>(hd.d_buf_v, hd.d_vals, d_vals, hd.nvals);
-  }
-  return cuda_status(cudaGetLastError(), "scatter_add_kernel");
+  // deterministic unpack once every slice is in: senders in ascending rank order
+  fo_status st2 = xp_group_end(h, [h, d_R, d_vals, s]() -> fo_status {
+    for (auto& hd : h->holders) {
+      if (d_R) scatter_add_kernel<<<grid_for(hd.nrows), 256, 0, s>>>(hd.d_buf_r, hd.d_rows, d_R, hd.nrows);
+      if (d_vals && hd.nvals > 0)
+        scatter_add_kernel<<<grid_for(hd.nvals), 256, 0, s>>>(hd.d_buf_v, hd.d_vals, d_vals, hd.nvals);
+    }
+    return cuda_status(cudaGetLastError(), "scatter_add_kernel");
+  });
+  return st ? st : st2;
 }
 
 fo_status fo_halo_info(fo_halo h, int32_t* n_neighbors, int64_t* recv_rows, int64_t* recv_vals) {

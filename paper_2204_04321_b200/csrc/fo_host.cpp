@@ -395,10 +395,15 @@ fo_status fo_plan_check_host(int64_t n_vert, const double* xy, int64_t n_tri, co
 
 fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, double Q) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
-  if (m->d_T) cudaSetDevice(m->device);
-  cudaFree(m->d_T);
-  m->d_T = nullptr;
-  if (!T_star) return FO_OK;
+  fo_status st = cuda_status(cudaSetDevice(m->device), "cudaSetDevice");
+  if (st) return st;
+  if (!T_star) {   // revert to the constant-A / A_elem path
+    cudaFree(m->d_T);
+    m->d_T = nullptr;
+    return FO_OK;
+  }
+  // validate and build the new field first: a rejected call leaves the
+  // previous temperature field (and the Arrhenius constants) in place
   if (!(A0 > 0.0)) return fail(FO_EINVAL, "A0 must be > 0");
   constexpr double kGasR = 8.314462618;   // J mol^-1 K^-1 (CODATA 2018)
   const int32_t L = m->L;
@@ -409,14 +414,17 @@ fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double A0, do
       if (!(v > 0.0)) return fail(FO_EINVAL, "T_star must be > 0 K");
       T[size_t(t * L + k)] = v;
     }
+  double* d_new = nullptr;
+  if (!T.empty()) {
+    st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&d_new), T.size() * sizeof(double)), "cudaMalloc");
+    if (!st) st = cuda_status(cudaMemcpy(d_new, T.data(), T.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
+    if (st) { cudaFree(d_new); return st; }
+  }
+  cudaFree(m->d_T);
+  m->d_T = d_new;
   m->A0fac = std::pow(A0, -1.0 / m->p.glen_n);
   m->QnR = Q / (m->p.glen_n * kGasR);
-  if (T.empty()) return FO_OK;
-  cudaSetDevice(m->device);
-  fo_status st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_T), T.size() * sizeof(double)), "cudaMalloc");
-  if (!st) st = cuda_status(cudaMemcpy(m->d_T, T.data(), T.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
-  if (st) { cudaFree(m->d_T); m->d_T = nullptr; }
-  return st;
+  return FO_OK;
 }
 
 fo_status fo_params_default(fo_params* p) {
@@ -569,7 +577,9 @@ fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, do
   fo_status st = cuda_status(cudaSetDevice(m->device), "cudaSetDevice");
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!m->d_stage_U && m->n_dof > 0) {
+  if (!m->d_stage_R && m->n_dof > 0) {   // keyed on the last allocation
+    cudaFree(m->d_stage_U);
+    m->d_stage_U = nullptr;
     st = cuda_status(cudaMalloc(&m->d_stage_U, sizeof(double) * m->n_dof), "cudaMalloc");
     if (!st) st = cuda_status(cudaMalloc(&m->d_stage_R, sizeof(double) * m->n_dof), "cudaMalloc");
     if (st) return st;

@@ -524,14 +524,14 @@ static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPl
 
 template <bool NEED_J, bool N3, bool TET>
 static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
-  static bool attr_set = false;
+  // the shared-memory opt-in is per device: set it on every call (cheap), so
+  // meshes on different devices of one process, and concurrent callers, are safe
   const size_t sm = smem_bytes(NEED_J);
-  if (!attr_set) {
+  {
     fo_status st = cuda_status(cudaFuncSetAttribute(ka_patch_kernel<NEED_J, N3, TET>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
                                "cudaFuncSetAttribute");
     if (st) return st;
-    attr_set = true;
   }
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
               m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};

@@ -207,7 +207,10 @@ __global__ void update_kernel(int64_t n, int kv, const double* __restrict__ V, i
 }
 
 fo_status ensure_solver_data(fo_mesh m) {
-  if (m->d_nbr) return FO_OK;
+  // keyed on the LAST allocation: a call that failed half way is redone
+  if (m->d_kry_work) return FO_OK;
+  cudaFree(m->d_nbr_ptr); cudaFree(m->d_self_slot); cudaFree(m->d_nbr); cudaFree(m->d_line_fac);
+  m->d_nbr_ptr = nullptr; m->d_self_slot = nullptr; m->d_nbr = nullptr; m->d_line_fac = nullptr;
   const int64_t nk = m->nA + m->nB;
   std::vector<int32_t> self(static_cast<size_t>(nk));
   for (int64_t c = 0; c < nk; ++c) {

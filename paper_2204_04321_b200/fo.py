@@ -73,6 +73,7 @@ _SIGS = {
     "fo_kernel_time_ms": [P, P, P],
     "fo_nccl_unique_id": [P],
     "fo_halo_create": [P, P, P, I32, I32, P],
+    "fo_halo_create_loopback": [P, P, I32, P],
     "fo_halo_import": [P, P, P],
     "fo_halo_sum": [P, P, P, P],
     "fo_halo_info": [P, P, P, P],
@@ -219,15 +220,30 @@ def nccl_unique_id() -> bytes:
 
 
 class Halo:
-    """NCCL ghost import / ghost-row sum of a partitioned mesh (collective)."""
+    """Ghost import / ghost-row sum of a partitioned mesh: NCCL (collective,
+    one rank per GPU) or, with Halo.loopback, all parts in one process."""
 
-    def __init__(self, mesh: "Mesh", uid: bytes, rank: int, n_ranks: int):
+    def __init__(self, mesh: "Mesh", uid: bytes | None, rank: int, n_ranks: int, _handle=None):
         self.mesh = mesh
+        if _handle is not None:
+            self.handle = _handle
+            return
         buf = (C.c_char * 128).from_buffer_copy(uid)
         h = C.c_void_p()
         check(lib().fo_halo_create(mesh.handle, mesh.graph().handle, buf, rank, n_ranks, C.byref(h)),
               "fo_halo_create")
         self.handle = h
+
+    @classmethod
+    def loopback(cls, meshes) -> list["Halo"]:
+        """fo_halo_create_loopback: the halos of all parts (meshes[p] = part p)
+        of one partition on one device."""
+        n = len(meshes)
+        parts = (C.c_void_p * n)(*[m.handle.value for m in meshes])
+        graphs = (C.c_void_p * n)(*[m.graph().handle.value for m in meshes])
+        out = (C.c_void_p * n)()
+        check(lib().fo_halo_create_loopback(parts, graphs, n, out), "fo_halo_create_loopback")
+        return [cls(m, None, p, n, _handle=C.c_void_p(out[p])) for p, m in enumerate(meshes)]
 
     def info(self):
         nn, rr, rv = C.c_int32(), C.c_int64(), C.c_int64()

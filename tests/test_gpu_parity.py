@@ -365,9 +365,11 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
 @pytest.mark.parametrize("P", [2, 3])
 def test_partitioned_assembly_with_halo_plan(torch_cuda, ora_mod, P, lateral):
     """local meshes of a P-way footprint partition (fo_mesh_create_part) on one
-    GPU, ghost-row partial sums added into the owners with the library's halo
-    plan (the data movement fo_halo_sum does over NCCL): owned rows equal the
-    single-domain assembly; ghost import fills the ghost U slices."""
+    GPU, ghost-row partial sums added into the owners with the library's host
+    halo plan (fo_halo_plan_host) applied here by index_add_: owned rows equal
+    the single-domain assembly, with and without the lateral term.  Ghost U is
+    copied from the global array here; the library's own fo_halo_import /
+    fo_halo_sum are tested in tests/test_gpu_halo.py."""
     import torch
     from paper_2204_04321_b200 import fo
     fp = mg.greenland_like(40.0, n_layers=5)
