@@ -8,12 +8,21 @@ Metric (BASELINE.json): "FO-Stokes Jacobian+residual assembly Melem/s per GPU,
   N = 1: config C3 (1-10 km graded footprint sized to the paper's 479,930
          triangles, P:596), 4.8 M wedges;
   N > 1: config C4, the C3 recipe refined to N x 479,930 triangles, footprint
-         partitioned into N Hilbert-contiguous parts (weak scaling), NCCL halo.
+         partitioned into N Hilbert-contiguous parts (weak scaling), NCCL halo;
+  --config C3 / C5 at N > 1: that mesh split into N parts (strong scaling,
+         BASELINE.json's "C3 ... 1 and 8 B200" and "C5 ... 8 B200" configs).
 value = all wedges of all ranks per second / 1e6 (Melem/s, whole job), timed
 with CUDA events around every step (L2 flushed between steps, outside the
-events), max over ranks.
+events), max over ranks; the line also carries the per-GPU figure (the
+metric's "per GPU") and, at N > 1, the scaling efficiency of P:531-535 against
+the one-GPU time of the base mesh measured in the same run.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config auto|C3|C4|C5] [--loopback P]
+
+--loopback P (N = 1): also time the P-part split of the workload on the one
+GPU through the library's halo path (fo_halo_import -> assemble every part ->
+fo_halo_sum, loopback transport): the multi-GPU code path end to end.
 
 --impl reference runs the CPU oracle (oracle/, the serial C++ FE assembly the
 CUDA path is validated against) on the host cores, rank 0 only.
@@ -49,6 +58,10 @@ def parse_args():
     ap.add_argument("--ref-sample-tris", type=int, default=3000, help="reference-arm sample per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--config", default="auto", choices=["auto", "C3", "C4", "C5"],
+                    help="auto: C3 at N = 1, C4 x N (weak) at N > 1; C3 / C5: strong scaling at N > 1")
+    ap.add_argument("--loopback", type=int, default=0, help="N = 1: also time P parts through the halo path")
+    ap.add_argument("--no-eta", action="store_true", help="N > 1: skip the one-GPU base run of the efficiency")
     return ap.parse_args()
 
 
@@ -61,11 +74,48 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload(n_gpus: int):
+def workload(n_gpus: int, config: str = "auto"):
+    """(footprint, config name, scaling, base config of the efficiency)"""
     from paper_2204_04321_b200 import meshgen as mg
-    if n_gpus == 1:
-        return mg.greenland_like_1_10(), "C3"
-    return mg.greenland_like_1_10(scale=float(n_gpus)), f"C4x{n_gpus}"
+    if config == "C5":
+        return mg.antarctica_like(), "C5", ("strong" if n_gpus > 1 else "weak"), "C5"
+    if config == "C3" or (config == "auto" and n_gpus == 1):
+        return mg.greenland_like_1_10(), "C3", ("strong" if n_gpus > 1 else "weak"), "C3"
+    return mg.greenland_like_1_10(scale=float(n_gpus)), f"C4x{n_gpus}", "weak", "C3"
+
+
+def scaling_efficiency(t1_ms: float, n1: int, tn_ms: float, nn: int, n: int) -> float:
+    """eta = ((t_1 / N_1) / (t_n / N_n)) / n, N = wedges
+    (weak scaling: N_n = n N_1, perfect eta = 1 at t_n = t_1; strong scaling:
+    N_n = N_1, perfect at t_n = t_1 / n)."""
+    return (t1_ms / n1) / (tn_ms / nn) / n
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def kernel_src_hash() -> str:
+    """sha256 (16 hex) of the CUDA/C++ sources and the build flags: an ncu
+    capture summary carries the hash of the build it measured, and bench flags
+    a capture taken on other kernel code."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2204_04321_b200", "csrc")
+    for f in sorted(glob.glob(os.path.join(csrc, "*"))):
+        if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+            h.update(os.path.basename(f).encode())
+            h.update(open(f, "rb").read())
+    h.update(os.environ.get("FO_EXTRA_NVCC_FLAGS", "").encode())
+    return h.hexdigest()[:16]
 
 
 class ClockSampler:
@@ -128,13 +178,17 @@ def algorithmic_bytes(n_elem, nnz, n_nodes, n_cols, n_tri, has_A):
 
 
 def ncu_summary(config_name):
-    """dram traffic / fp64 counts of the dominant kernel from the committed ncu capture."""
+    """dram traffic / fp64 counts of the dominant kernel from the committed ncu
+    capture; `matches_build` says whether it was taken on these kernel sources."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d if d.get("config") == config_name else None
+    if d.get("config") != config_name:
+        return None
+    d["matches_build"] = d.get("src_hash") == kernel_src_hash()
+    return d
 
 
 def roofline_entry(alg_bytes, kernel_ms, kernel_ms_total, step_ms_total, n_elems, peak_gbs, peak_src, prof,
@@ -172,8 +226,11 @@ def roofline_entry(alg_bytes, kernel_ms, kernel_ms_total, step_ms_total, n_elems
     if prof:
         roof["ncu"] = {k: prof.get(k) for k in ("fp64_pipe_pct", "registers_per_thread", "warps_active_pct",
                                                  "l1_data_pipe_pct", "shared_wavefronts", "shared_bank_conflicts",
-                                                 "l2_red_sectors_per_s") if prof.get(k) is not None}
-        roof["ncu"]["spills"] = 0   # ptxas -v of the build
+                                                 "l2_red_sectors_per_s", "src_hash", "matches_build")
+                       if prof.get(k) is not None}
+        if not prof.get("matches_build", False):
+            roof["ncu"]["stale"] = ("capture taken on other kernel sources: flop_per_wedge and traffic "
+                                    "are the captured build's")
     return roof
 
 
@@ -228,18 +285,29 @@ def oracle_parallel(fp, n_tri_sample, procs, reps=1):
     return per_rep, nt, nt * fp.n_layers
 
 
-def cpu_baseline_oracle(fp, n_tri_sample_per_core):
+ORACLE_COMPILER = "g++ -O2 -std=c++17 (no fast-math, no threads), oracle/fo_oracle.cpp"
+
+
+def cpu_baseline_oracle(fp, n_tri_sample_per_core, one_core_tris=6000):
     """The oracle as it stands (serial C++ per process, Dual<12> AD Jacobian) on
     every host core: a sample of n_tri_sample_per_core triangles per core (the
-    whole workload if smaller), split into Hilbert-contiguous parts."""
+    whole workload if smaller), split into Hilbert-contiguous parts; plus the
+    1-core figure of SURVEY.md 8(d) d5 (one process, median of 3 calls after a
+    warm-up, on the first one_core_tris triangles)."""
     cores = _host_cores()
     secs, nt, nw = oracle_parallel(fp, n_tri_sample_per_core * cores, cores)
     dt = secs[0]
+    s1, nt1, nw1 = oracle_parallel(fp, one_core_tris, 1, reps=4)
+    t1 = statistics.median(s1[1:])
     return {"value": nw / dt / 1e6, "unit": "Melem/s", "cores": cores, "kind": "oracle",
             "sample": f"first {nt} triangles x {fp.n_layers} layers = {nw} wedges of {fp.name}, split into "
                       f"{cores} Hilbert-contiguous parts, one oracle process per core (R + Dual<12> AD "
                       f"Jacobian, -O2); wall time of the slowest process {dt:.2f} s",
-            "seconds": dt}
+            "seconds": dt,
+            "one_core": {"value": nw1 / t1 / 1e6, "unit": "Melem/s", "cores": 1,
+                         "sample": f"first {nt1} triangles x {fp.n_layers} layers = {nw1} wedges, one process, "
+                                   f"median of 3 calls after a warm-up", "seconds": t1},
+            "cpu_model": cpu_model(), "compiler": ORACLE_COMPILER}
 
 
 def run_reference(args):
@@ -248,7 +316,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    fp, name = workload(args.gpus)
+    fp, name, scaling, _ = workload(args.gpus, args.config)
     cores = _host_cores()
     secs, nt, nw = oracle_parallel(fp, args.ref_sample_tris * cores, cores, reps=args.warmup + args.steps)
     times = secs[args.warmup:]
@@ -258,13 +326,93 @@ def run_reference(args):
               f"one oracle process per core, R + Dual<12> AD Jacobian")
     line = {"metric": METRIC, "value": value, "unit": "Melem/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{name}: {fp.name}, sample of {nt} triangles x {fp.n_layers} layers",
                        "n_elem": nw},
-            "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model(), "compiler": ORACLE_COMPILER},
             "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def time_steps(step, steps, flush, stream):
+    """CUDA-event time of each of `steps` calls of step() on `stream`, the L2
+    flushed (512 MB written) before each, outside the events; ms per step."""
+    import torch
+    evs = []
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def single_gpu_base(fp, steps, warmup, dev, flush, stream):
+    """the one-GPU time of the efficiency's base mesh (single domain, same protocol)"""
+    import torch
+    from paper_2204_04321_b200 import fo
+    m = fo.Mesh.from_footprint(fp, device=dev.index)
+    g = m.graph()
+    U = torch.tensor(fp.U, dtype=torch.float64, device=dev)
+    R = torch.empty(m.n_dofs, dtype=torch.float64, device=dev)
+    V = torch.empty(g.nnz, dtype=torch.float64, device=dev)
+    for _ in range(max(warmup, 3)):
+        m.jacobian(U, g, R, V)
+    ms = time_steps(lambda: m.jacobian(U, g, R, V), steps, flush, stream)
+    n = m.n_elems
+    del R, V, U, g
+    m.close()
+    return sum(ms) / len(ms), n
+
+
+def loopback_run(fp, P, steps, warmup, dev, flush, stream):
+    """--loopback P: the workload split into P parts on this one GPU, every
+    step = fo_halo_import on every part -> fo_assemble_jacobian on every part
+    -> fo_halo_sum on every part (loopback transport: the library's halo plans,
+    staging, gather / unpack-add kernels; device copies for the transfers)."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    L1 = fp.n_layers + 1
+    part = fo.partition(fp.n_tri, P)
+    meshes = [fo.Mesh.from_footprint(fp, device=dev.index, part=part, my_part=p, n_parts=P) for p in range(P)]
+    halos = fo.Halo.loopback(meshes)
+    Ug = fp.U.reshape(fp.n_vert, L1, 2)
+    st = []
+    for m in meshes:
+        g = m.graph()
+        st.append((m, g, torch.tensor(Ug[m.columns()[0]].reshape(-1), device=dev),
+                   torch.empty(m.n_dofs, dtype=torch.float64, device=dev),
+                   torch.empty(g.nnz, dtype=torch.float64, device=dev)))
+
+    def step():
+        for h, (m, g, U, R, V) in zip(halos, st):
+            h.import_(U)
+        for m, g, U, R, V in st:
+            m.jacobian(U, g, R, V)
+        for h, (m, g, U, R, V) in zip(halos, st):
+            h.sum(R, V)
+
+    for _ in range(max(warmup, 3)):
+        step()
+    ms = time_steps(step, steps, flush, stream)
+    t = sum(ms) / len(ms)
+    recv = [h.info() for h in halos]
+    out = {"parts": P, "ms_per_step": t, "value": fp.n_elem / (t / 1e3) / 1e6, "unit": "Melem/s",
+           "halo_values_received_per_step": int(sum(r[1] + r[2] for r in recv)),
+           "max_neighbours": int(max(r[0] for r in recv)),
+           "note": "P parts of the workload on one GPU through fo_halo_import / fo_assemble_jacobian / "
+                   "fo_halo_sum with the loopback transport (the multi-GPU code path, one device)"}
+    for h in halos:
+        h.close()
+    for m, g, U, R, V in st:
+        m.close()
+    return out
 
 
 def main():
@@ -290,7 +438,7 @@ def main():
     if world > 1:
         dist.barrier()
 
-    fp, cfg_name = workload(world)
+    fp, cfg_name, scaling, base_cfg = workload(world, args.config)
     L = fp.n_layers
     if world == 1:
         mesh = fo.Mesh.from_footprint(fp, device=local)
@@ -372,6 +520,9 @@ def main():
     prof = ncu_summary(cfg_name)
     roof = roofline_entry(alg, kavg, kern_ms, sum(step_ms), mesh.n_elems, peak, peak_src, prof,
                           "ka_patch_kernel" if args.scatter == 0 else "assemble_atomic_kernel")
+    res = _build.ptxas_resources("ka_patch_kernelILb1ELb1ELb0E" if args.scatter == 0 else "assemble_atomic_kernelILb1ELb1E")
+    if res is not None:
+        roof["ptxas"] = {"registers_per_thread": res[0], "spill_bytes": res[1], "source": "ptxas -v of this build"}
 
     # residual only (KR), the same timing protocol
     r_ms = []
@@ -475,6 +626,27 @@ def main():
                "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * (n_owned + owned_vals),
                "api": "torch H2D of owned U -> fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum -> D2H owned rows"}
 
+    # N > 1: the efficiency of P:531-535 against the base mesh on one GPU, timed
+    # by rank 0 in this run with the same protocol (C3 for the weak series)
+    eta = None
+    if world > 1 and not args.no_eta:
+        dist.barrier()
+        if rank == 0:
+            from paper_2204_04321_b200 import meshgen as mg
+            fb = fp if base_cfg == cfg_name else (mg.greenland_like_1_10() if base_cfg == "C3" else mg.antarctica_like())
+            t1, n1 = single_gpu_base(fb, args.steps, args.warmup, dev, flush, stream)
+            tn = tot_ms / args.steps
+            eta = {"eta": scaling_efficiency(t1, n1, tn, elems, world), "scaling": scaling,
+                   "t1_ms": t1, "n1_wedges": n1, "tn_ms": tn, "nn_wedges": elems, "n": world,
+                   "base": f"{base_cfg} single domain on GPU 0 of this run",
+                   "formula": "((t1/N1)/(tn/Nn))/n, N = wedges (PAPER.md P:531-535)"}
+        dist.barrier()
+
+    loop = None
+    if world == 1 and args.loopback > 1:
+        loop = loopback_run(fp, args.loopback, args.steps, args.warmup, dev, flush, stream)
+        loop["vs_single_domain"] = (tot_ms / args.steps) / loop["ms_per_step"]
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_oracle(fp, args.cpu_sample_tris)
@@ -485,12 +657,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Melem/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Greenland-like footprint, SIA velocity; SURVEY.md 8(d) d1)",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded " + ("Antarctica" if cfg_name == "C5" else "Greenland") +
+                    "-like footprint, SIA velocity; SURVEY.md 8(d) d1)",
+            "per_gpu": {"value": value / world, "unit": "Melem/s per GPU",
+                        "note": "the metric's per-GPU figure (value = whole job over all GPUs)"},
+            "scaling_efficiency": eta, "loopback": loop,
             "config": {"workload": f"{cfg_name}: {fp.name}, {fp.n_tri} triangles x {L} layers = "
                                    f"{fp.n_elem} wedges, {world} part(s)",
                        "wedges_per_gpu": mesh.n_elems, "nnz_per_gpu": graph.nnz, "n_dofs_per_gpu": mesh.n_dofs,
                        "parallelism": f"footprint partition x{world}" + (", NCCL halo" if world > 1 else ""),
+                       "config": cfg_name,
                        "scatter": "owner-computes" if args.scatter == 0 else "atomic",
                        "l2": "1.7 GB of CSR values written per step (> 126 MB L2) and a 512 MB buffer "
                              "written between timed steps"},

@@ -57,12 +57,16 @@ __device__ __forceinline__ void trace(int slot) {
 #define FO_TRACE_AT(s)
 #endif
 
-// one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor)
+// one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor):
+// bulk_init by one thread, a CTA barrier, then bulk_load by that thread
+__device__ __forceinline__ void bulk_init(uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
@@ -378,11 +382,12 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
     sp.ncols = c1 - c0; sp.npairs = q1 - q0;
     sp.nedge = __ldg(pv.nedge + p);
+    if (threadIdx.x == 0) bulk_init(&plan_bar);
+    // the mbarrier is initialised before any warp can wait on it (warps without
+    // triangles reach the first bulk_wait at once) and before the copy arrives on it
+    __syncthreads();
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
-  // the mbarrier is initialised before any warp can wait on it (warps without
-  // triangles reach the first bulk_wait at once)
-  __syncthreads();
 #ifdef FO_STAGGER_NS
   // experiment: the second CTA of each SM in the first wave starts late, so
   // the two resident CTAs alternate their element and gather phases

@@ -5,9 +5,13 @@ usage: python tools/ncu_summary.py X.ncu-rep CONFIG N_WEDGES [out.json]"""
 import csv
 import io
 import json
+import os
 import re
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402  (kernel_src_hash: the capture records the build it measured)
 
 rep, cfg, nw = sys.argv[1], sys.argv[2], float(sys.argv[3])
 out = sys.argv[4] if len(sys.argv) > 4 else "profiles/ncu_summary.json"
@@ -45,6 +49,12 @@ d = {"config": cfg, "kernel": h and v[h.index("Kernel Name")] if "Kernel Name" i
      "fp64_instr_per_wedge": {k: c / nw for k, c in cnt.items()},
      "fp64_flop_per_wedge": flops / nw}
 d["dram_bytes_per_launch"] = d["dram_bytes_read"] + d["dram_bytes_write"]
+d["src_hash"] = bench.kernel_src_hash()
+try:
+    d["git_head"] = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                                   text=True).stdout.strip() or None
+except OSError:
+    d["git_head"] = None
 
 
 def raw(name):
