@@ -238,10 +238,16 @@ FO_API fo_status fo_krylov_update(fo_mesh m, int64_t n, int32_t k, const double*
 FO_API fo_status fo_set_lateral(fo_mesh m, int enable);
 
 /* Scatter strategy of fo_assemble_jacobian (ablation; default FO_SCATTER_OWNER):
- * FO_SCATTER_OWNER  column-patch owner-computes kernel: every CSR value written
- *                   exactly once with plain stores (deterministic, no zero-fill);
- * FO_SCATTER_ATOMIC one thread per wedge, fp64 atomics into zeroed outputs. */
-typedef enum { FO_SCATTER_OWNER = 0, FO_SCATTER_ATOMIC = 1 } fo_scatter;
+ * FO_SCATTER_OWNER    column-patch owner-computes kernel: every CSR value of an
+ *                     interior column written exactly once with plain stores
+ *                     (deterministic); for wedges the warp-specialised kernel
+ *                     (element warpgroup with TMEM scratch + scatter warpgroup)
+ * FO_SCATTER_ATOMIC   one thread per wedge, fp64 atomics into zeroed outputs
+ * FO_SCATTER_OWNER_WS the warp-specialised kernel explicitly (wedges, R + J)
+ * FO_SCATTER_OWNER_1WG the round-1 single-warpgroup patch kernel (element and
+ *                     scatter phases alternate in the same threads). */
+typedef enum { FO_SCATTER_OWNER = 0, FO_SCATTER_ATOMIC = 1, FO_SCATTER_OWNER_WS = 2,
+               FO_SCATTER_OWNER_1WG = 3 } fo_scatter;
 FO_API fo_status fo_set_scatter(fo_mesh m, fo_scatter s);
 
 /* Kernel launches the last assembly call enqueued (for bench accounting). */

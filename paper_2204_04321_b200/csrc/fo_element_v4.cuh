@@ -42,6 +42,15 @@
 
 namespace fo {
 
+// D layout (shared level-k diagonal block of the patch kernels): the three
+// off-diagonal 2x2 node blocks (j < j2) first, row-major [a][b], at
+// 4 (j + j2 - 1); then the three diagonal node blocks (a <= b) at
+// 12 + 3 j + a + b; the residual at 21 + 2 j + a.
+__host__ __device__ constexpr int dmap(int p, int p2) {
+  return (p >> 1) == (p2 >> 1) ? 12 + 3 * (p >> 1) + (p & 1) + (p2 & 1)
+                               : 4 * ((p >> 1) + (p2 >> 1) - 1) + 2 * (p & 1) + (p2 & 1);
+}
+
 __host__ __device__ constexpr int pk6(int p, int q) {
   return p <= q ? p * 6 - (p * (p - 1)) / 2 + (q - p) : q * 6 - (q * (q - 1)) / 2 + (p - q);
 }

@@ -618,7 +618,7 @@ fo_status fo_set_element(fo_mesh m, fo_element type) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
   if (m->quad) return fail(FO_EINVAL, "a quadrilateral mesh always uses hexahedra");
   if (type != FO_ELEM_WEDGE && type != FO_ELEM_TET3) return fail(FO_EINVAL, "unknown element type");
-  if (type == FO_ELEM_TET3 && (m->lateral || m->scatter != FO_SCATTER_OWNER))
+  if (type == FO_ELEM_TET3 && (m->lateral || (m->scatter != FO_SCATTER_OWNER && m->scatter != FO_SCATTER_OWNER_1WG)))
     return fail(FO_EINVAL, "FO_ELEM_TET3 needs the owner scatter and no lateral term");
   if (type == m->elem_type) return FO_OK;
   // The tetrahedral element runs with every triangle's corners in global-id
@@ -658,10 +658,11 @@ fo_status fo_set_element(fo_mesh m, fo_element type) {
 
 fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
+  if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC && s != FO_SCATTER_OWNER_WS && s != FO_SCATTER_OWNER_1WG)
+    return fail(FO_EINVAL, "bad scatter");
   if (m->quad && s != FO_SCATTER_OWNER) return fail(FO_EINVAL, "hexahedra use the coloured scatter");
-  if (s != FO_SCATTER_OWNER && m->elem_type != FO_ELEM_WEDGE)
-    return fail(FO_EINVAL, "the atomic scatter supports FO_ELEM_WEDGE only");
-  if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC) return fail(FO_EINVAL, "bad scatter");
+  if (s != FO_SCATTER_OWNER && s != FO_SCATTER_OWNER_1WG && m->elem_type != FO_ELEM_WEDGE)
+    return fail(FO_EINVAL, "this scatter supports FO_ELEM_WEDGE only");
   m->scatter = s;
   return FO_OK;
 }

@@ -88,7 +88,7 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->quad) return launch_hex(m, d_U, d_R, nullptr, s);
-  if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
+  if (m->scatter != FO_SCATTER_ATOMIC && m->plan.n_patches > 0) {
     st = launch_owner(m, d_U, d_R, nullptr, s);
   } else {
     st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
@@ -108,7 +108,7 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
   m->last_launches = 0;
   if (m->n_dof == 0) return FO_OK;
   if (m->quad) return launch_hex(m, d_U, d_R, d_vals, s);
-  if (m->scatter == FO_SCATTER_OWNER && m->plan.n_patches > 0) {
+  if (m->scatter != FO_SCATTER_ATOMIC && m->plan.n_patches > 0) {
     st = launch_owner(m, d_U, d_R, d_vals, s);
   } else {
     if (d_R) st = cuda_status(cudaMemsetAsync(d_R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");

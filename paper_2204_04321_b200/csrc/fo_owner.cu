@@ -23,6 +23,7 @@
 #include "fo_element.cuh"
 #include "fo_element_v4.cuh"
 #include "fo_element_tet.cuh"
+#include "fo_element_ws.cuh"
 
 #include <type_traits>
 #include "fo_internal.h"
@@ -92,13 +93,6 @@ constexpr int kDR = 6;
 constexpr int kPlanOffsetR = ((kDR + kC) * TP * 8 + 15) / 16 * 16;
 constexpr int kPatchCtasPerSmR = 3;
 
-// D layout: the three off-diagonal 2x2 node blocks (j < j2) first, row-major
-// [a][b], at 4 (j + j2 - 1); then the three diagonal node blocks (a <= b) at
-// 12 + 3 j + a + b; the residual at 21 + 2 j + a.
-__host__ __device__ constexpr int dmap(int p, int p2) {
-  return (p >> 1) == (p2 >> 1) ? 12 + 3 * (p >> 1) + (p & 1) + (p2 & 1)
-                               : 4 * ((p >> 1) + (p2 >> 1) - 1) + 2 * (p & 1) + (p2 & 1);
-}
 
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
@@ -228,11 +222,11 @@ __device__ __forceinline__ void emit(const PlanPair& pp, const PlanCol& pc, cons
 template <bool UP>
 __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, const double* D,
                                           const double* O, double* __restrict__ vals,
-                                          double* __restrict__ partials) {
+                                          double* __restrict__ partials, int tid, int nthr) {
   // edge pairs (exactly two entries) first, then self pairs (one entry per
   // fan triangle, padded to even); a variant gathering two edge pairs per
   // thread at a time measured slower (1.98 vs 1.91 ms)
-  for (int pi = threadIdx.x; pi < sp.npairs; pi += blockDim.x) {
+  for (int pi = tid; pi < sp.npairs; pi += nthr) {
     const PlanPair pp = sp.pairs[pi];
     PairSums s;
     const uint32_t* cp = sp.contrib + pp.off - 2;   // even count >= 2, 8-byte aligned
@@ -248,8 +242,9 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
 
 // Dr: the residual slots (D + 21 TP in the R + J layout, the whole D of KR)
 __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, const double* Dr,
-                                          double* __restrict__ R, double* __restrict__ partials) {
-  for (int ci = threadIdx.x; ci < sp.ncols; ci += blockDim.x) {
+                                          double* __restrict__ R, double* __restrict__ partials, int tid,
+                                          int nthr) {
+  for (int ci = tid; ci < sp.ncols; ci += nthr) {
     const PlanCol& pc = sp.cols[ci];
     double r0, r1;
     {   // self lists hold >= 2 entries (padded to even): first step r = a + b
@@ -279,12 +274,13 @@ __device__ __forceinline__ void phase_b_r(const SmemPlan& sp, int kk, int L, con
 template <bool NEED_J>
 __device__ __forceinline__ void phase_b(const SmemPlan& sp, int kk, int L, const double* D,
                                         const double* O, double* __restrict__ R,
-                                        double* __restrict__ vals, double* __restrict__ partials) {
+                                        double* __restrict__ vals, double* __restrict__ partials,
+                                        int tid, int nthr) {
   if (NEED_J) {
-    if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals, partials);
-    else phase_b_j<false>(sp, kk, L, D, O, vals, partials);
+    if (kk < L) phase_b_j<true>(sp, kk, L, D, O, vals, partials, tid, nthr);
+    else phase_b_j<false>(sp, kk, L, D, O, vals, partials, tid, nthr);
   }
-  phase_b_r(sp, kk, L, NEED_J ? D + 21 * TP : D, R, partials);
+  phase_b_r(sp, kk, L, NEED_J ? D + 21 * TP : D, R, partials, tid, nthr);
 }
 
 // Sink of wedge_element_v4: bottom parts added to D and O in shared memory,
@@ -439,7 +435,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     __syncthreads();
     FO_TRACE_AT(2 + 2 * k);
 #ifndef FO_EXPERIMENT_NO_PHASE_B
-    phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials);
+    phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials, threadIdx.x, blockDim.x);
 #endif
     __syncthreads();
     FO_TRACE_AT(3 + 2 * k);
@@ -455,11 +451,157 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   }
   if (L == 0) bulk_wait(&plan_bar);
   __syncthreads();
-  phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials);
+  phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials, threadIdx.x, blockDim.x);
 #ifdef FO_TRACE
   __syncthreads();
   FO_TRACE_AT(2 + 2 * L);
 #endif
+}
+
+// ---------------------------------------------------------------------------
+// KA-ws: the warp-specialised patch kernel ("KA-ws").
+// Same patch plan, shared layout and scatter (phase B) as ka_patch_kernel, but
+// the element and scatter phases run in two warpgroups that overlap:
+//   WG0 (threads 0..127, one per triangle, up to kWsRegsE registers): wedge
+//        element k+1 (fo_element_ws.cuh) with all its intermediate blocks in
+//        the thread's private TMEM row, while
+//   WG1 (threads 128..255, kWsRegsB registers): phase B of level k from the
+//        shared D / O arrays.
+// Handshake per level with two named barriers of 256 threads: EMPTY (WG1
+// arrives after its phase B; WG0 waits before overwriting D / O) and FULL (WG0
+// arrives after publishing D(k) / O(k); WG1 waits before its phase B).
+constexpr int kWsThreads = 256;
+#ifndef FO_WS_REGS_E
+#define FO_WS_REGS_E 208
+#endif
+constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;   // setmaxnreg split: E + B = 2 x 128
+constexpr int kPlanOffsetWS = ((kD + kO) * TP * 8 + 15) / 16 * 16;
+constexpr int kBarEmpty = 1, kBarFull = 2, kBarElem = 3;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool N3>
+__global__ void __launch_bounds__(kWsThreads, 2)
+ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
+             const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp, PlanView pv,
+             const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
+  extern __shared__ __align__(16) double smem[];
+  double* const D = smem;              // [kD][TP]
+  double* const O = smem + kD * TP;    // [kO][TP]
+  __shared__ uint64_t plan_bar;
+  __shared__ uint32_t tmem_base;
+  const int p = blockIdx.x;
+  const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
+  SmemPlan sp;
+  char* const base = reinterpret_cast<char*>(smem) + kPlanOffsetWS;
+  const int64_t b0 = __ldg(pv.blob_off + p), b1 = __ldg(pv.blob_off + p + 1);
+  {
+    const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
+    const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
+    sp.pairs = reinterpret_cast<const PlanPair*>(base);
+    sp.cols = reinterpret_cast<const PlanCol*>(base + (q1 - q0) * sizeof(PlanPair));
+    sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
+    sp.ncols = c1 - c0; sp.npairs = q1 - q0;
+    sp.nedge = __ldg(pv.nedge + p);
+  }
+  if (threadIdx.x == 0) bulk_init(&plan_bar);
+  if (threadIdx.x < 32) tmem::alloc(&tmem_base, kTmCols);   // warp 0 owns the TMEM allocation
+  {   // triangle slot kPatchTris: the zero column the plan's pad entries read
+    const int i = int(threadIdx.x) - 128;
+    if (i >= 0 && i < kD) D[i * TP + kPatchTris] = 0.0;
+    if (i >= 0 && i < kO) O[i * TP + kPatchTris] = 0.0;
+  }
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
+  const int L = kp.L;
+  if (threadIdx.x < 128) {
+    // ---------------- WG0: elements ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsE));
+    const int tl = threadIdx.x;
+    const bool active = tl < nt;
+    // tcgen05.ld / st are warp-collective: lanes without a triangle evaluate a
+    // copy of the patch's last one and publish nothing
+    const int te = active ? tl : nt - 1;
+    const uint32_t tm = tmem_base + (uint32_t(tl & ~31) << 16);   // this warp's TMEM lane quarter
+    TriRec tr;
+    {
+      const int* tp = reinterpret_cast<const int*>(tris + (t0 + te));
+      const int2 v01 = __ldg(reinterpret_cast<const int2*>(tp));
+      tr.v[0] = v01.x; tr.v[1] = v01.y; tr.v[2] = __ldg(tp + 2);
+    }
+    {
+      double z[27];
+#pragma unroll
+      for (int i = 0; i < 27; ++i) z[i] = 0.0;
+      tmem::st<27>(tm + kTmHeld, z);   // no wedge below the bed
+    }
+    for (int k = 0; k < L; ++k) {
+      double acc[36];
+      {
+        const ColRec* colk = col;
+        asm volatile("" : "+l"(colk));
+        TriGeo geo;
+        load_tri_geo(colk, tr, geo);
+        const double Afac = wedge_afac(kp, Aw, t0 + te, k);
+        WedgeIn w;
+        wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
+#ifndef FO_EXPERIMENT_WS_NO_ELEMENT
+        wedge_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
+#else
+#pragma unroll
+        for (int i = 0; i < 36; ++i) acc[i] = w.zb[i % 3] * w.ub[i % 3];
+#endif
+      }
+      double dk[27];
+      tmem::wait_st();
+      tmem::ld<27>(tm + kTmBB, dk);
+      named_sync(kBarEmpty, kWsThreads);   // phase B of level k-1 has released D / O
+      if (active) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+#pragma unroll
+          for (int q2 = 0; q2 < 6; ++q2) O[(6 * q + q2) * TP + tl] = acc[oidx(q, q2)];
+#pragma unroll
+        for (int i = 0; i < kD; ++i) D[i * TP + tl] = dk[i];
+      }
+      named_arrive(kBarFull, kWsThreads);   // level k published
+    }
+    {   // the surface level L: D(L) = the top block of wedge L-1
+      double hd[27];
+      tmem::wait_st();
+      tmem::ld<27>(tm + kTmHeld, hd);
+      named_sync(kBarEmpty, kWsThreads);
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < kD; ++i) D[i * TP + tl] = hd[i];
+      }
+      named_arrive(kBarFull, kWsThreads);
+    }
+    tmem::fence_before();
+    named_sync(kBarElem, 128);   // every element warp is done with TMEM
+    tmem::fence_after();
+    if (tl < 32) tmem::dealloc(tmem_base, kTmCols);
+  } else {
+    // ---------------- WG1: scatter (phase B) ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsB));
+    const int tb = int(threadIdx.x) - 128;
+    bulk_wait(&plan_bar);
+    named_arrive(kBarEmpty, kWsThreads);   // D / O start free
+    for (int kk = 0; kk <= L; ++kk) {
+      named_sync(kBarFull, kWsThreads);
+#ifndef FO_EXPERIMENT_WS_NO_PHASE_B
+      phase_b<true>(sp, kk, L, D, O, R, vals, pv.partials, tb, 128);
+#endif
+      if (kk < L) named_arrive(kBarEmpty, kWsThreads);
+    }
+  }
 }
 
 // zero the rows (CSR values and residual) of boundary columns
@@ -527,6 +669,29 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
 
 static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
+template <bool N3>
+static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
+  const size_t sm = size_t(kPlanOffsetWS) + kPlanBytes;
+  fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(sm)), "cudaFuncSetAttribute");
+  if (st) return st;
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
+              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (m->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  ka_ws_kernel<N3><<<m->plan.n_patches, kWsThreads, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A,
+                                                           make_kparams(m), pv, U, R, vals);
+  if (m->timing) {
+    cudaEventRecord(e1, s);
+    m->timed.push_back({e0, e1});
+  }
+  return cuda_status(cudaGetLastError(), "ka_ws_kernel launch");
+}
+
 template <bool NEED_J, bool N3, bool TET>
 static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
   // the shared-memory opt-in is per device: set it on every call (cheap), so
@@ -584,7 +749,12 @@ fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals
   }
   const bool n3 = m->p.glen_n == 3.0;
   fo_status st;
-  if (need_j)
+  // wedge R + J: the warp-specialised kernel unless the round-1 kernel is asked for
+  const bool ws = need_j && m->elem_type == FO_ELEM_WEDGE &&
+                  (m->scatter == FO_SCATTER_OWNER || m->scatter == FO_SCATTER_OWNER_WS);
+  if (ws)
+    st = n3 ? launch_ws<true>(m, d_U, R, d_vals, s) : launch_ws<false>(m, d_U, R, d_vals, s);
+  else if (need_j)
     st = m->elem_type == FO_ELEM_TET3
              ? (n3 ? launch_patch<true, true, true>(m, d_U, R, d_vals, s) : launch_patch<true, false, true>(m, d_U, R, d_vals, s))
              : (n3 ? launch_patch<true, true, false>(m, d_U, R, d_vals, s) : launch_patch<true, false, false>(m, d_U, R, d_vals, s));

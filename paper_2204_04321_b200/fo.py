@@ -23,7 +23,7 @@ ROOT = os.path.dirname(_PKG)
 HEADER = os.path.join(ROOT, "include", "fo.h")
 
 FO_OK, FO_EINVAL, FO_EMESH, FO_ECUDA, FO_ENCCL, FO_ENOMEM, FO_ESTATE = 0, -1, -2, -3, -4, -5, -6
-SCATTER_OWNER, SCATTER_ATOMIC = 0, 1
+SCATTER_OWNER, SCATTER_ATOMIC, SCATTER_OWNER_WS, SCATTER_OWNER_1WG = 0, 1, 2, 3
 _NAMES = {0: "FO_OK", -1: "FO_EINVAL", -2: "FO_EMESH", -3: "FO_ECUDA", -4: "FO_ENCCL",
           -5: "FO_ENOMEM", -6: "FO_ESTATE"}
 

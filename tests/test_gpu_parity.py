@@ -64,7 +64,7 @@ def check_parity(o, g, params=None, fp=None, terms=None):
     return err.max(initial=0) / max(np.abs(vals).max(initial=1.0), 1e-300)
 
 
-SCATTERS = [0, 1]
+SCATTERS = [0, 1, 2, 3]   # owner (default), atomic, warp-specialised owner, round-1 owner
 
 
 @pytest.mark.parametrize("scatter", SCATTERS)
