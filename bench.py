@@ -53,7 +53,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scatter", type=int, default=0, help="0 owner-computes (default), 1 atomic")
+    ap.add_argument("--scatter", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="0 owner-computes (default: the warp-specialised kernel), 1 atomic, 2 warp-specialised, 3 round-1 patch kernel")
     ap.add_argument("--cpu-sample-tris", type=int, default=40000, help="oracle sample per host core")
     ap.add_argument("--ref-sample-tris", type=int, default=3000, help="reference-arm sample per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -177,7 +178,13 @@ def algorithmic_bytes(n_elem, nnz, n_nodes, n_cols, n_tri, has_A):
     return 8 * nnz + 16 * n_nodes + 16 * n_nodes + 40 * n_cols + 12 * n_tri + (8 * n_elem if has_A else 0)
 
 
-def ncu_summary(config_name):
+# the R + J assembly kernel each --scatter mode launches (name in the ncu
+# launch list, mangled-name fragment in the ptxas log)
+DOMINANT_KERNEL = {0: ("ka_ws_kernel", "ka_ws_kernelILb1E"), 1: ("assemble_atomic_kernel", "assemble_atomic_kernelILb1ELb1E"),
+                   2: ("ka_ws_kernel", "ka_ws_kernelILb1E"), 3: ("ka_patch_kernel", "ka_patch_kernelILb1ELb1ELb0E")}
+
+
+def ncu_summary(config_name, kernel_name=None):
     """dram traffic / fp64 counts of the dominant kernel from the committed ncu
     capture; `matches_build` says whether it was taken on these kernel sources."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -187,6 +194,8 @@ def ncu_summary(config_name):
         d = json.load(f)
     if d.get("config") != config_name:
         return None
+    if kernel_name is not None and kernel_name not in d.get("kernel", ""):
+        return None   # a capture of another kernel says nothing about this one
     d["matches_build"] = d.get("src_hash") == kernel_src_hash()
     return d
 
@@ -517,10 +526,10 @@ def main():
     has_A = fp.A_elem is not None
     alg = algorithmic_bytes(mesh.n_elems, graph.nnz, mesh.n_nodes, n_cols, n_tri_local, has_A)
     kavg = kern_ms / max(kern_n, 1)
-    prof = ncu_summary(cfg_name)
-    roof = roofline_entry(alg, kavg, kern_ms, sum(step_ms), mesh.n_elems, peak, peak_src, prof,
-                          "ka_patch_kernel" if args.scatter == 0 else "assemble_atomic_kernel")
-    res = _build.ptxas_resources("ka_patch_kernelILb1ELb1ELb0E" if args.scatter == 0 else "assemble_atomic_kernelILb1ELb1E")
+    kname, ksym = DOMINANT_KERNEL[args.scatter]
+    prof = ncu_summary(cfg_name, kname)
+    roof = roofline_entry(alg, kavg, kern_ms, sum(step_ms), mesh.n_elems, peak, peak_src, prof, kname)
+    res = _build.ptxas_resources(ksym)
     if res is not None:
         roof["ptxas"] = {"registers_per_thread": res[0], "spill_bytes": res[1], "source": "ptxas -v of this build"}
 
@@ -668,7 +677,7 @@ def main():
                        "wedges_per_gpu": mesh.n_elems, "nnz_per_gpu": graph.nnz, "n_dofs_per_gpu": mesh.n_dofs,
                        "parallelism": f"footprint partition x{world}" + (", NCCL halo" if world > 1 else ""),
                        "config": cfg_name,
-                       "scatter": "owner-computes" if args.scatter == 0 else "atomic",
+                       "scatter": {0: "owner-computes", 1: "atomic", 2: "owner-computes (ws)", 3: "owner-computes (round-1 kernel)"}[args.scatter],
                        "l2": "1.7 GB of CSR values written per step (> 126 MB L2) and a 512 MB buffer "
                              "written between timed steps"},
             "roofline": roof, "residual_only": residual_only, "graph_100": graph100, "e2e": e2e,

@@ -85,6 +85,12 @@ def test_ncu_capture_staleness_is_flagged(tmp_path, monkeypatch):
     r = bench.roofline_entry(1.77e9, 1.6, 16.0, 18.0, 4_800_000, 6500.0, "m", p, "k")
     assert "stale" not in r["ncu"]
     assert bench.ncu_summary("C5") is None
+    # a capture of another kernel (e.g. the residual-only instance) is not used
+    assert bench.ncu_summary("C3", "ka_ws_kernel") is None
+    prof["kernel"] = "void fo::ka_ws_kernel<true>(...)"
+    (d / "ncu_summary.json").write_text(json.dumps(prof))
+    assert bench.ncu_summary("C3", "ka_ws_kernel") is not None
+    assert bench.DOMINANT_KERNEL[0][0] == "ka_ws_kernel"
 
 
 def test_kernel_src_hash_tracks_flags(monkeypatch):

@@ -339,6 +339,12 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
     vals = vals.cpu().numpy()
     rng = mg.SplitMix64(77)
     cols = np.unique((rng.uniform(48) * fp.n_vert).astype(np.int64))
+    _check_full_size_columns(ora_mod, fp, cols, rp, vals, (R, Rr))
+
+
+def _check_full_size_columns(ora_mod, fp, cols, rp, vals, Rs):
+    """complete rows of the columns `cols` of a full-size assembly against the
+    oracle on the sub-footprint of their triangle fans"""
     fan = np.nonzero(np.isin(fp.tri, cols).any(axis=1))[0]
     sub = mg.sub_footprint_tris(fp, fan)
     o = ora_mod.Oracle(sub)
@@ -353,12 +359,53 @@ def test_c3_full_size_sampled(torch_cuda, ora_mod, cfg):
             for a in range(2):
                 r_g = 2 * (c * L1 + k) + a
                 r_o = 2 * (lc * L1 + k) + a
-                assert abs(R[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
-                assert abs(Rr[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
+                for Rx in Rs:
+                    assert abs(Rx[r_g] - Ro[r_o]) <= R_TOL * np.abs(Mo).max()
                 seg_g = vals[rp[r_g]:rp[r_g + 1]]
                 seg_o = ov[orp[r_o]:orp[r_o + 1]]
                 assert seg_g.size == seg_o.size
                 assert np.abs(seg_g - seg_o).max() <= J_TOL * np.abs(seg_o).max()
+
+
+def _patch_classes(fp, patch_tris=128):
+    """per column: the number of patches of the owner-computes plan whose
+    triangles touch it (1 interior, 2 boundary, >= 3 multi), from the plan's
+    equal-size ranges of <= patch_tris consecutive triangles (fo_plan.cpp)"""
+    nt = fp.n_tri
+    np0 = (nt + patch_tris - 1) // patch_tris
+    bounds = (np.arange(np0 + 1, dtype=np.int64) * nt) // np0
+    patch = np.searchsorted(bounds, np.arange(nt), side="right") - 1
+    pairs = np.unique(np.stack([fp.tri.reshape(-1).astype(np.int64), np.repeat(patch, 3)], axis=1), axis=0)
+    return np.bincount(pairs[:, 0], minlength=fp.n_vert)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_full_size_targeted_columns(torch_cuda, ora_mod, cfg):
+    """at full size in the bench's launch configuration,
+    deliberately sample the scatter's hard cases -- columns touched by >= 3
+    patches (the multi fix-up path), patch-boundary columns (zero fill + RED),
+    the highest-degree column and its neighbours, and interior columns -- with
+    complete rows (R + J kernel and residual-only kernel) against the oracle."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.antarctica_like() if cfg == "C5" else mg.greenland_like_1_10()
+    mesh = fo.Mesh.from_footprint(fp)
+    U = torch.tensor(fp.U, device="cuda")
+    g = mesh.graph()
+    R, vals = mesh.jacobian(U)
+    Rr = mesh.residual(U)
+    torch.cuda.synchronize()
+    rp, _ = g.to_host()
+    npatch = _patch_classes(fp)
+    deg = np.bincount(fp.tri.reshape(-1), minlength=fp.n_vert)
+    rng = mg.SplitMix64(91)
+    pick = lambda ids, n: ids[(rng.uniform(n) * ids.size).astype(np.int64)] if ids.size else ids
+    top = int(np.argmax(deg))
+    nbr = np.unique(fp.tri[(fp.tri == top).any(axis=1)])
+    multi, bnd, inner = (np.nonzero(npatch >= 3)[0], np.nonzero(npatch == 2)[0], np.nonzero(npatch == 1)[0])
+    assert multi.size and bnd.size and inner.size
+    cols = np.unique(np.concatenate([pick(multi, 12), pick(bnd, 12), pick(inner, 6), nbr]))
+    _check_full_size_columns(ora_mod, fp, cols, rp, vals.cpu().numpy(), (R.cpu().numpy(), Rr.cpu().numpy()))
 
 
 @pytest.mark.parametrize("lateral", [False, True])

@@ -52,3 +52,19 @@ def test_plan_c3_statistics():
     assert 0.30 < st["zero_cols"] / fp.n_vert < 0.45
     assert 0.01 < st["multi"] / fp.n_vert < 0.06
     assert st["plan_bytes"] <= 233472 // 2
+
+
+@pytest.mark.parametrize("case", ["C2", "C3"])
+def test_patch_classes_match_the_plan(case):
+    """the GPU test's column classes (tests/test_gpu_parity._patch_classes:
+    patches touching each column) agree with the library's plan: columns
+    touched by >= 2 patches are its zero-filled boundary columns, by >= 3 its
+    multi columns -- so the targeted full-size parity samples what it claims.
+    The plan halves the few ranges whose plan exceeds the shared-memory budget,
+    which only ADDS boundaries: the classes are a lower bound, within 0.5%."""
+    from test_gpu_parity import _patch_classes
+    fp = mg.greenland_like(16.0) if case == "C2" else mg.greenland_like_1_10()
+    st = fo.plan_check_host(fp.xy, fp.tri, fp.n_layers)
+    npatch = _patch_classes(fp)
+    for got, want in ((int((npatch >= 2).sum()), st["zero_cols"]), (int((npatch >= 3).sum()), st["multi"])):
+        assert want * 0.995 <= got <= want
