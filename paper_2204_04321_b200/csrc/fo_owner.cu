@@ -472,9 +472,11 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
 // arrives after publishing D(k) / O(k); WG1 waits before its phase B).
 constexpr int kWsThreads = 256;
 #ifndef FO_WS_REGS_E
-#define FO_WS_REGS_E 208
+#define FO_WS_REGS_E 200
 #endif
-constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;   // setmaxnreg split: E + B = 2 x 128
+// setmaxnreg split: E + B = 2 x 128.  200 / 56: no spills in either warpgroup
+// (208 / 48 spilled the scatter's addresses: C3 1.471 vs 1.403 ms; 192 / 64: 1.496)
+constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;
 constexpr int kPlanOffsetWS = ((kD + kO) * TP * 8 + 15) / 16 * 16;
 constexpr int kBarEmpty = 1, kBarFull = 2, kBarElem = 3;
 
