@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--config", default="auto", choices=["auto", "C3", "C4", "C5"],
                     help="auto: C3 at N = 1, C4 x N (weak) at N > 1; C3 / C5: strong scaling at N > 1")
     ap.add_argument("--loopback", type=int, default=0, help="N = 1: also time P parts through the halo path")
+    ap.add_argument("--halo", choices=["fused", "sequential"], default="fused",
+                    help="N > 1: fo_assemble_jacobian_halo (export overlapped with the interior patches, "
+                         "default) or fo_assemble_jacobian then fo_halo_sum")
     ap.add_argument("--no-eta", action="store_true", help="N > 1: skip the one-GPU base run of the efficiency")
     return ap.parse_args()
 
@@ -399,7 +402,7 @@ def loopback_run(fp, P, steps, warmup, dev, flush, stream):
                    torch.empty(m.n_dofs, dtype=torch.float64, device=dev),
                    torch.empty(g.nnz, dtype=torch.float64, device=dev)))
 
-    def step():
+    def step_seq():
         for h, (m, g, U, R, V) in zip(halos, st):
             h.import_(U)
         for m, g, U, R, V in st:
@@ -407,16 +410,28 @@ def loopback_run(fp, P, steps, warmup, dev, flush, stream):
         for h, (m, g, U, R, V) in zip(halos, st):
             h.sum(R, V)
 
-    for _ in range(max(warmup, 3)):
-        step()
-    ms = time_steps(step, steps, flush, stream)
-    t = sum(ms) / len(ms)
+    def step_fused():
+        for h, (m, g, U, R, V) in zip(halos, st):
+            h.import_(U)
+        for h, (m, g, U, R, V) in zip(halos, st):
+            h.assemble(U, R, V)
+
+    res = {}
+    for name, step in (("sequential", step_seq), ("fused", step_fused)):
+        for _ in range(max(warmup, 3)):
+            step()
+        ms = time_steps(step, steps, flush, stream)
+        t = sum(ms) / len(ms)
+        res[name] = {"ms_per_step": t, "value": fp.n_elem / (t / 1e3) / 1e6}
     recv = [h.info() for h in halos]
-    out = {"parts": P, "ms_per_step": t, "value": fp.n_elem / (t / 1e3) / 1e6, "unit": "Melem/s",
+    out = {"parts": P, "ms_per_step": res["fused"]["ms_per_step"], "value": res["fused"]["value"],
+           "unit": "Melem/s", "sequential": res["sequential"], "fused": res["fused"],
            "halo_values_received_per_step": int(sum(r[1] + r[2] for r in recv)),
            "max_neighbours": int(max(r[0] for r in recv)),
-           "note": "P parts of the workload on one GPU through fo_halo_import / fo_assemble_jacobian / "
-                   "fo_halo_sum with the loopback transport (the multi-GPU code path, one device)"}
+           "note": "P parts of the workload on one GPU with the loopback transport (the multi-GPU code path, "
+                   "one device): sequential = fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum on every "
+                   "part; fused = fo_halo_import -> fo_assemble_jacobian_halo (ghost rows sent while the "
+                   "interior patches run)"}
     for h in halos:
         h.close()
     for m, g, U, R, V in st:
@@ -473,10 +488,14 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        if halo is not None:
-            halo.import_(U)
-        mesh.jacobian(U, graph, R, V)
-        if halo is not None:
+        if halo is None:
+            mesh.jacobian(U, graph, R, V)
+            return
+        halo.import_(U)
+        if args.halo == "fused":   # fo_assemble_jacobian_halo: ghost rows sent while the interior runs
+            halo.assemble(U, R, V)
+        else:
+            mesh.jacobian(U, graph, R, V)
             halo.sum(R, V)
 
     for _ in range(max(args.warmup, 3)):
@@ -525,7 +544,9 @@ def main():
     peak, peak_src = measured_peaks()
     has_A = fp.A_elem is not None
     alg = algorithmic_bytes(mesh.n_elems, graph.nnz, mesh.n_nodes, n_cols, n_tri_local, has_A)
-    kavg = kern_ms / max(kern_n, 1)
+    # per STEP: a fused halo step (N > 1) launches the kernel twice (boundary
+    # and interior patches), each over part of the patches
+    kavg = kern_ms / max(args.steps, 1)
     kname, ksym = DOMINANT_KERNEL[args.scatter]
     prof = ncu_summary(cfg_name, kname)
     roof = roofline_entry(alg, kavg, kern_ms, sum(step_ms), mesh.n_elems, peak, peak_src, prof, kname)
@@ -542,10 +563,14 @@ def main():
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        if halo is not None:
+        if halo is None:
+            mesh.residual(U, R)
+        elif args.halo == "fused":
             halo.import_(U)
-        mesh.residual(U, R)
-        if halo is not None:
+            halo.assemble(U, R)
+        else:
+            halo.import_(U)
+            mesh.residual(U, R)
             halo.sum(R, None)
         b.record(stream)
         r_ms.append((a, b))
@@ -633,7 +658,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": elems * len(tms) / (float(t.item()) / 1e3) / 1e6, "unit": "Melem/s",
                "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * (n_owned + owned_vals),
-               "api": "torch H2D of owned U -> fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum -> D2H owned rows"}
+               "api": "torch H2D of owned U -> fo_halo_import -> fo_assemble_jacobian_halo (or fo_assemble_jacobian + "
+                      "fo_halo_sum with --halo sequential) -> D2H owned rows"}
 
     # N > 1: the efficiency of P:531-535 against the base mesh on one GPU, timed
     # by rank 0 in this run with the same protocol (C3 for the weak series)
@@ -675,7 +701,7 @@ def main():
             "config": {"workload": f"{cfg_name}: {fp.name}, {fp.n_tri} triangles x {L} layers = "
                                    f"{fp.n_elem} wedges, {world} part(s)",
                        "wedges_per_gpu": mesh.n_elems, "nnz_per_gpu": graph.nnz, "n_dofs_per_gpu": mesh.n_dofs,
-                       "parallelism": f"footprint partition x{world}" + (", NCCL halo" if world > 1 else ""),
+                       "parallelism": f"footprint partition x{world}" + (f", NCCL halo ({args.halo})" if world > 1 else ""),
                        "config": cfg_name,
                        "scatter": {0: "owner-computes", 1: "atomic", 2: "owner-computes (ws)", 3: "owner-computes (round-1 kernel)"}[args.scatter],
                        "l2": "1.7 GB of CSR values written per step (> 126 MB L2) and a 512 MB buffer "

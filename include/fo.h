@@ -287,6 +287,23 @@ FO_API fo_status fo_halo_import(fo_halo h, double* d_U, void* stream);
  * the owned prefix of d_R / d_vals is complete (ghost rows unspecified).
  * Either pointer may be NULL. */
 FO_API fo_status fo_halo_sum(fo_halo h, double* d_R, double* d_vals, void* stream);
+/* Assembly and Export in one call, overlapped:
+ * R = F(U) and, if d_vals != NULL, the Jacobian values of the local (part)
+ * mesh, then the ghost-row sum of fo_halo_sum -- with the patches holding the
+ * ghost-touching triangles (a part mesh orders them first) computed on the
+ * halo's own higher-priority stream, and their rows sent to the owners while
+ * the interior patches are still being computed on `stream`.  Same results
+ * as fo_assemble_jacobian (or fo_assemble_residual) followed by fo_halo_sum,
+ * bit for bit.  The ghost U must be current (fo_halo_import before).  Falls
+ * back to that sequential order for one part, the atomic scatter and the
+ * lateral term (which adds into ghost rows after every patch).  All work is
+ * joined into `stream` on return.  d_U[n_dofs], d_R[n_dofs] (not NULL),
+ * d_vals[nnz] or NULL (residual only; g may then be NULL).  With the loopback
+ * transport the same phase rule as fo_halo_sum applies.  Errors: FO_EINVAL
+ * (NULL mesh / halo / U / R, hexahedral mesh), FO_ESTATE (graph or halo built
+ * for another mesh), FO_ECUDA, FO_ENCCL. */
+FO_API fo_status fo_assemble_jacobian_halo(fo_mesh m, fo_graph g, fo_halo h, const double* d_U, double* d_R,
+                                           double* d_vals, void* stream);
 /* halo plan sizes: neighbours, ghost DOFs received, values received */
 FO_API fo_status fo_halo_info(fo_halo h, int32_t* n_neighbors, int64_t* recv_rows, int64_t* recv_vals);
 

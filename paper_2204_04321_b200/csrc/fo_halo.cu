@@ -186,6 +186,10 @@ struct fo_halo_s {
   };
   std::vector<Owner> owners;
   std::vector<Holder> holders;
+  // fo_assemble_jacobian_halo: the boundary patches and the transfers run on
+  // `side` (higher priority than the caller's stream), joined back by events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev0 = nullptr, ev_b = nullptr, ev_sum = nullptr;
 };
 
 namespace fo {
@@ -397,6 +401,47 @@ fo_status halo_plan(fo_halo h, fo_mesh local) {
   }
   return st;
 }
+fo_status halo_streams(fo_halo h) {
+  int lo = 0, hi = 0;
+  fo_status st = cuda_status(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+  if (!st) st = cuda_status(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi), "cudaStreamCreate");
+  for (cudaEvent_t* e : {&h->ev0, &h->ev_b, &h->ev_sum})
+    if (!st) st = cuda_status(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+  return st;
+}
+
+// Export: send my ghost slices of R / CSR values to their owners and
+// add the slices I receive into my owned rows, senders in ascending rank
+// order.  Transfers go on `sx`; the unpack-add on `su` once they are in
+// (joined by an event when the streams differ).
+fo_status halo_sum_impl(fo_halo h, double* d_R, double* d_vals, cudaStream_t sx, cudaStream_t su) {
+  fo_status st = xp_group_start(h);
+  for (auto& o : h->owners) {
+    if (st) break;
+    if (d_R) st = xp_send(h, d_R + o.row0, o.nrows, o.q, sx);
+    if (!st && d_vals && o.nvals > 0) st = xp_send(h, d_vals + o.val0, o.nvals, o.q, sx);
+  }
+  for (auto& hd : h->holders) {
+    if (st) break;
+    if (d_R) st = xp_recv(h, hd.d_buf_r, hd.nrows, hd.p, sx);
+    if (!st && d_vals && hd.nvals > 0) st = xp_recv(h, hd.d_buf_v, hd.nvals, hd.p, sx);
+  }
+  // deterministic unpack once every slice is in: senders in ascending rank order
+  fo_status st2 = xp_group_end(h, [h, d_R, d_vals, sx, su]() -> fo_status {
+    if (su != sx) {
+      fo_status e = cuda_status(cudaEventRecord(h->ev_sum, sx), "cudaEventRecord");
+      if (!e) e = cuda_status(cudaStreamWaitEvent(su, h->ev_sum, 0), "cudaStreamWaitEvent");
+      if (e) return e;
+    }
+    for (auto& hd : h->holders) {
+      if (d_R) scatter_add_kernel<<<grid_for(hd.nrows), 256, 0, su>>>(hd.d_buf_r, hd.d_rows, d_R, hd.nrows);
+      if (d_vals && hd.nvals > 0)
+        scatter_add_kernel<<<grid_for(hd.nvals), 256, 0, su>>>(hd.d_buf_v, hd.d_vals, d_vals, hd.nvals);
+    }
+    return cuda_status(cudaGetLastError(), "scatter_add_kernel");
+  });
+  return st ? st : st2;
+}
 }  // namespace
 }  // namespace fo
 
@@ -425,6 +470,7 @@ fo_status fo_halo_create(fo_mesh local, fo_graph local_g, const void* nccl_uniqu
       std::memcpy(&id, nccl_unique_id, sizeof(id));
       st = nccl_status(ncclCommInitRank(&h->comm, n_ranks, id, rank), "ncclCommInitRank");
     }
+    if (!st) st = halo_streams(h);
     if (st) { fo_halo_destroy(h); return st; }
   }
   *out = h;
@@ -458,6 +504,7 @@ fo_status fo_halo_create_loopback(const fo_mesh* parts, const fo_graph* graphs, 
     h->loop = G;
     out[p] = h;
     if (n_parts > 1) st = halo_plan(h, parts[p]);
+    if (!st && n_parts > 1) st = halo_streams(h);
   }
   if (st)
     for (int32_t p = 0; p < n_parts; ++p) { fo_halo_destroy(out[p]); out[p] = nullptr; }
@@ -490,27 +537,31 @@ fo_status fo_halo_sum(fo_halo h, double* d_R, double* d_vals, void* stream) {
   fo_status st = cuda_status(cudaSetDevice(h->device), "cudaSetDevice");
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = xp_group_start(h);
-  for (auto& o : h->owners) {
-    if (st) break;
-    if (d_R) st = xp_send(h, d_R + o.row0, o.nrows, o.q, s);
-    if (!st && d_vals && o.nvals > 0) st = xp_send(h, d_vals + o.val0, o.nvals, o.q, s);
+  return halo_sum_impl(h, d_R, d_vals, s, s);
+}
+
+fo_status fo_assemble_jacobian_halo(fo_mesh m, fo_graph g, fo_halo h, const double* d_U, double* d_R,
+                                    double* d_vals, void* stream) {
+  if (!m || !h) return fail(FO_EINVAL, "mesh or halo is NULL");
+  if (!d_U || !d_R) return fail(FO_EINVAL, "d_U or d_R is NULL");
+  if (d_vals && (!g || g->mesh != m)) return fail(FO_ESTATE, "graph is NULL or was built for another mesh");
+  if (h->rank != m->part || h->n_ranks != m->n_parts) return fail(FO_ESTATE, "halo was built for another mesh");
+  if (m->quad) return fail(FO_EINVAL, "fo_assemble_jacobian_halo: wedge / tetrahedral meshes only");
+  fo_status st = cuda_status(cudaSetDevice(m->device), "cudaSetDevice");
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // sequential fallbacks: one part; the atomic ablation; the lateral term (it
+  // adds into ghost rows after every patch, so nothing can be sent earlier)
+  if (h->n_ranks == 1 || m->scatter == FO_SCATTER_ATOMIC || m->lateral || m->plan.n_patches == 0) {
+    st = d_vals ? launch_jacobian(m, d_U, d_R, d_vals, s) : launch_residual(m, d_U, d_R, s);
+    if (!st && h->n_ranks > 1) st = halo_sum_impl(h, d_R, d_vals, s, s);
+    return st;
   }
-  for (auto& hd : h->holders) {
-    if (st) break;
-    if (d_R) st = xp_recv(h, hd.d_buf_r, hd.nrows, hd.p, s);
-    if (!st && d_vals && hd.nvals > 0) st = xp_recv(h, hd.d_buf_v, hd.nvals, hd.p, s);
-  }
-  // deterministic unpack once every slice is in: senders in ascending rank order
-  fo_status st2 = xp_group_end(h, [h, d_R, d_vals, s]() -> fo_status {
-    for (auto& hd : h->holders) {
-      if (d_R) scatter_add_kernel<<<grid_for(hd.nrows), 256, 0, s>>>(hd.d_buf_r, hd.d_rows, d_R, hd.nrows);
-      if (d_vals && hd.nvals > 0)
-        scatter_add_kernel<<<grid_for(hd.nvals), 256, 0, s>>>(hd.d_buf_v, hd.d_vals, d_vals, hd.nvals);
-    }
-    return cuda_status(cudaGetLastError(), "scatter_add_kernel");
-  });
-  return st ? st : st2;
+  st = launch_owner_overlap(m, d_U, d_R, d_vals, s, h->side, h->ev0, h->ev_b);
+  if (st) return st;
+  // the ghost rows are final on `side` (ev_b): send them while the interior
+  // patches run on s; the unpack-add joins s after both
+  return halo_sum_impl(h, d_R, d_vals, h->side, s);
 }
 
 fo_status fo_halo_info(fo_halo h, int32_t* n_neighbors, int64_t* recv_rows, int64_t* recv_vals) {
@@ -537,6 +588,9 @@ void fo_halo_destroy(fo_halo h) {
     cudaFree(hd.d_imp_idx); cudaFree(hd.d_imp_buf);
   }
   if (h->comm) ncclCommDestroy(h->comm);
+  if (h->side) cudaStreamDestroy(h->side);
+  for (cudaEvent_t e : {h->ev0, h->ev_b, h->ev_sum})
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 

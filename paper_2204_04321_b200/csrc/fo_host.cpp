@@ -164,6 +164,30 @@ fo_status build_topology(int64_t n_vert, int64_t n_tri, const int32_t* tri, int3
     for (int i = 0; i < 3; ++i) T.tri.push_back(int32_t(loc[tri[3 * t + i]]));
   }
   const int64_t nt = int64_t(T.tri_glob.size());
+  // part meshes: the local triangles touching a ghost (class B) column lead,
+  // each group in its original (Hilbert) order -- the patches holding them
+  // come first, so fo_assemble_jacobian_halo can send the ghost rows while
+  // the remaining (interior) patches are computed
+  T.n_bnd_tri = 0;
+  if (part) {
+    std::vector<int64_t> bnd, rest;
+    for (int64_t t = 0; t < nt; ++t) {
+      bool g = false;
+      for (int i = 0; i < 3; ++i) g = g || (T.tri[size_t(3 * t + i)] >= T.nA);
+      (g ? bnd : rest).push_back(t);
+    }
+    T.n_bnd_tri = int64_t(bnd.size());
+    bnd.insert(bnd.end(), rest.begin(), rest.end());
+    std::vector<int32_t> tri2(T.tri.size());
+    std::vector<int64_t> glob2(T.tri_glob.size());
+    for (int64_t i = 0; i < nt; ++i) {
+      const int64_t t = bnd[size_t(i)];
+      glob2[size_t(i)] = T.tri_glob[size_t(t)];
+      for (int j = 0; j < 3; ++j) tri2[size_t(3 * i + j)] = T.tri[size_t(3 * t + j)];
+    }
+    T.tri.swap(tri2);
+    T.tri_glob.swap(glob2);
+  }
   // coupling lists
   std::vector<std::vector<int32_t>> lists(size_t(T.nA + T.nB));
   for (int64_t i = 0; i < T.nA; ++i) {
@@ -341,6 +365,7 @@ host_topology:
   m->nbr = std::move(T.nbr);
   m->colstart = std::move(T.colstart);
   m->trirec = std::move(T.trirec);
+  m->n_bnd_tri = T.n_bnd_tri;
 
   if (host_only) {   // the patch plan only, nothing on a device (fo_plan_check_host)
     st = build_patch_plan(m, false);

@@ -100,6 +100,10 @@ struct PatchPlan {
   std::vector<MultiRec> multi;       // columns touched by >= 3 patches
   std::vector<int32_t> nedge;        // [n_patches] leading edge pairs (two entries each)
   int32_t n_partials = 0;
+  // part meshes: patches [0, n_bnd_patches) hold every triangle touching a
+  // ghost column; multi records [0, n_multi_bnd) are touched by those patches only
+  int32_t n_bnd_patches = 0;
+  int32_t n_multi_bnd = 0;
 };
 
 struct DevPatch {
@@ -126,6 +130,7 @@ struct fo_mesh_s {
   int32_t L = 0;
   int64_t n_col = 0, nA = 0, nB = 0, nC = 0;  // local columns by class
   int64_t n_tri = 0;                          // local triangles
+  int64_t n_bnd_tri = 0;                      // of which the leading ones touch a ghost column
   int64_t n_node = 0, n_dof = 0, n_elem = 0, n_owned_dof = 0;
   int64_t nnz = 0;
   // host topology (kept for graph / halo construction)
@@ -203,6 +208,7 @@ struct Topo {
   std::vector<int32_t> nbr;
   std::vector<int64_t> colstart;
   std::vector<TriRec> trirec;
+  int64_t n_bnd_tri = 0;          // leading local triangles touching a ghost column
 };
 fo_status build_topology(int64_t n_vert, int64_t n_tri, const int32_t* tri, int32_t L,
                          const int32_t* part, int32_t my_part, Topo& T);
@@ -215,6 +221,9 @@ fo_status launch_residual(fo_mesh m, const double* d_U, double* d_R, void* strea
 fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_vals,
                           void* stream);
 fo_status build_patch_plan(fo_mesh m, bool upload = true);
+// owner-computes assembly pieces (fo_owner.cu)
+fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
+                               cudaStream_t side, cudaEvent_t ev0, cudaEvent_t ev_b);
 void free_patch_plan(fo_mesh m);
 fo_status plan_check(const fo_mesh m, int64_t* stats);
 // NEXT-f1 lateral margin term (fo_lateral.cu)

@@ -39,24 +39,9 @@ struct PlanView {
   const uint8_t* __restrict__ blob;      // per-patch plan blobs (fo_plan.cpp)
   const int64_t* __restrict__ blob_off;
   double* partials;   // multi columns' partial blocks (fo_plan.cpp)
+  int p_off;          // patch of block 0 (a launch covers patches p_off .. p_off + gridDim.x - 1)
 };
 
-#ifdef FO_TRACE
-// experiment: per-patch %globaltimer stamps (smid, start, then the end of
-// every phase A and phase B), read back by fo_debug_trace (tools/trace_phases.py)
-constexpr int kTraceSlots = 24, kTraceMax = 8192;
-__device__ unsigned long long g_trace[kTraceMax * kTraceSlots];
-__device__ __forceinline__ void trace(int slot) {
-  if (threadIdx.x == 0 && blockIdx.x < kTraceMax && slot < kTraceSlots) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_trace[blockIdx.x * kTraceSlots + slot] = t;
-  }
-}
-#define FO_TRACE_AT(s) trace(s)
-#else
-#define FO_TRACE_AT(s)
-#endif
 
 // one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor):
 // bulk_init by one thread, a CTA barrier, then bulk_load by that thread
@@ -108,13 +93,6 @@ struct SmemPlan {
 };
 
 __device__ __forceinline__ void put2(double* dst, double x, double y, bool interior) {
-#ifdef FO_EXPERIMENT_NO_RED
-  interior = true;
-#endif
-#ifdef FO_EXPERIMENT_NO_STORE
-  if (x == 1.2345e300 && y == -1.0) { *dst = x; }   // keep the sums alive, store nothing
-  return;
-#endif
   if (interior) {
     *reinterpret_cast<double2*>(dst) = make_double2(x, y);
   } else {
@@ -178,11 +156,6 @@ __device__ __forceinline__ void gather2(uint2 c2, const double* D, const double*
   }
 }
 
-__device__ __forceinline__ void zero_sums(PairSums& s) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) s.dg[i] = s.up[i] = s.nx[i] = 0.0;
-}
-
 // write one pair's sums: plain stores (interior column) or RED (boundary),
 // or the patch's partial block (self slot of a multi column)
 template <bool UP>
@@ -230,12 +203,8 @@ __device__ __forceinline__ void phase_b_j(const SmemPlan& sp, int kk, int L, con
     const PlanPair pp = sp.pairs[pi];
     PairSums s;
     const uint32_t* cp = sp.contrib + pp.off - 2;   // even count >= 2, 8-byte aligned
-#ifndef FO_EXPERIMENT_NO_GATHER
     gather2<UP, true>(make_uint2(pp.c0, pp.c1), D, O, s);
     for (int e = 2; e < pp.cnt; e += 2) gather2<UP, false>(*reinterpret_cast<const uint2*>(cp + e), D, O, s);
-#else
-    zero_sums(s);
-#endif
     emit<UP>(pp, sp.cols[pp.col], s, kk, L, vals, partials);
   }
 }
@@ -362,7 +331,7 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   double* const D = smem;                                       // [kD][TP] (KR: [kDR][TP])
   double* const O = smem + kD * TP;                             // [kO][TP] (KR: unused)
   double* const C = smem + (NEED_J ? kD + kO : kDR) * TP;       // [kC][TP]
-  const int p = blockIdx.x;
+  const int p = pv.p_off + int(blockIdx.x);
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   // the patch's plan -> shared memory (after the value buffers): one bulk
   // copy, issued now and waited for before the first gather phase
@@ -384,19 +353,6 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     __syncthreads();
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
-#ifdef FO_STAGGER_NS
-  // experiment: the second CTA of each SM in the first wave starts late, so
-  // the two resident CTAs alternate their element and gather phases
-  if (blockIdx.x >= 148 && blockIdx.x < 296) __nanosleep(FO_STAGGER_NS);
-#endif
-#ifdef FO_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[blockIdx.x * kTraceSlots] = smid;
-  }
-  FO_TRACE_AT(1);
-#endif
   const int L = kp.L;
   const int tl = threadIdx.x;
   const bool active = tl < nt;
@@ -433,12 +389,8 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     }
     if (k == 0) bulk_wait(&plan_bar);
     __syncthreads();
-    FO_TRACE_AT(2 + 2 * k);
-#ifndef FO_EXPERIMENT_NO_PHASE_B
     phase_b<NEED_J>(sp, k, L, D, O, R, vals, pv.partials, threadIdx.x, blockDim.x);
-#endif
     __syncthreads();
-    FO_TRACE_AT(3 + 2 * k);
     if (active) {   // the held top block becomes level k+1's diagonal block
       if (NEED_J) {
 #pragma unroll
@@ -452,10 +404,6 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   if (L == 0) bulk_wait(&plan_bar);
   __syncthreads();
   phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials, threadIdx.x, blockDim.x);
-#ifdef FO_TRACE
-  __syncthreads();
-  FO_TRACE_AT(2 + 2 * L);
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -497,7 +445,7 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   double* const O = smem + kD * TP;    // [kO][TP]
   __shared__ uint64_t plan_bar;
   __shared__ uint32_t tmem_base;
-  const int p = blockIdx.x;
+  const int p = pv.p_off + int(blockIdx.x);
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   SmemPlan sp;
   char* const base = reinterpret_cast<char*>(smem) + kPlanOffsetWS;
@@ -554,12 +502,7 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
         const double Afac = wedge_afac(kp, Aw, t0 + te, k);
         WedgeIn w;
         wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
-#ifndef FO_EXPERIMENT_WS_NO_ELEMENT
         wedge_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
-#else
-#pragma unroll
-        for (int i = 0; i < 36; ++i) acc[i] = w.zb[i % 3] * w.ub[i % 3];
-#endif
       }
       double dk[27];
       tmem::wait_st();
@@ -598,9 +541,7 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     named_arrive(kBarEmpty, kWsThreads);   // D / O start free
     for (int kk = 0; kk <= L; ++kk) {
       named_sync(kBarFull, kWsThreads);
-#ifndef FO_EXPERIMENT_WS_NO_PHASE_B
       phase_b<true>(sp, kk, L, D, O, R, vals, pv.partials, tb, 128);
-#endif
       if (kk < L) named_arrive(kBarEmpty, kWsThreads);
     }
   }
@@ -672,21 +613,21 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
 static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
 template <bool N3>
-static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
+static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np) {
   const size_t sm = size_t(kPlanOffsetWS) + kPlanBytes;
   fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sm)), "cudaFuncSetAttribute");
   if (st) return st;
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
-              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};
+              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials, p0};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  ka_ws_kernel<N3><<<m->plan.n_patches, kWsThreads, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A,
-                                                           make_kparams(m), pv, U, R, vals);
+  ka_ws_kernel<N3><<<np, kWsThreads, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R,
+                                              vals);
   if (m->timing) {
     cudaEventRecord(e1, s);
     m->timed.push_back({e0, e1});
@@ -695,7 +636,8 @@ static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, 
 }
 
 template <bool NEED_J, bool N3, bool TET>
-static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s) {
+static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0,
+                              int np) {
   // the shared-memory opt-in is per device: set it on every call (cheap), so
   // meshes on different devices of one process, and concurrent callers, are safe
   const size_t sm = smem_bytes(NEED_J);
@@ -706,15 +648,15 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
     if (st) return st;
   }
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
-              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials};
+              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials, p0};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  ka_patch_kernel<NEED_J, N3, TET><<<m->plan.n_patches, kPatchTris, sm, s>>>(
-      m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R, vals);
+  ka_patch_kernel<NEED_J, N3, TET><<<np, kPatchTris, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A,
+                                                              make_kparams(m), pv, U, R, vals);
   if (m->timing) {
     cudaEventRecord(e1, s);
     m->timed.push_back({e0, e1});
@@ -722,68 +664,127 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
   return cuda_status(cudaGetLastError(), "ka_patch_kernel launch");
 }
 
-fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s) {
-  const bool need_j = d_vals != nullptr;
+namespace {
+// The pieces of one owner-computes assembly: the
+// prologue (class-C residual zero, boundary-column zero fill), the patch
+// kernel over a range of patches, the multi-column fix-up over a range of
+// its records.
+struct OwnerCall {
+  fo_mesh m;
+  const double* U;
+  double* R;
+  double* vals;   // nullptr: residual only
+  int launches = 0;
+};
+
+fo_status owner_begin(OwnerCall& c, fo_mesh m, const double* d_U, double* d_R, double* d_vals) {
+  c.m = m;
+  c.U = d_U;
+  c.vals = d_vals;
   // R is always produced by the kernel; use a scratch vector when the caller passes none
-  double* R = d_R;
-  if (!R) {
+  c.R = d_R;
+  if (!c.R) {
     if (!m->d_scratch_R) {
       fo_status st = cuda_status(cudaMalloc(&m->d_scratch_R, sizeof(double) * m->n_dof), "cudaMalloc");
       if (st) return st;
     }
-    R = m->d_scratch_R;
+    c.R = m->d_scratch_R;
   }
-  int launches = 0;
+  return FO_OK;
+}
+
+fo_status owner_prologue(OwnerCall& c, cudaStream_t s) {
+  fo_mesh m = c.m;
   const int64_t nk_dof = 2 * (m->nA + m->nB) * (m->L + 1);
   if (nk_dof < m->n_dof) {   // column-only (class C) DOFs: residual 0
-    fo_status st = cuda_status(cudaMemsetAsync(R + nk_dof, 0, sizeof(double) * (m->n_dof - nk_dof), s),
+    fo_status st = cuda_status(cudaMemsetAsync(c.R + nk_dof, 0, sizeof(double) * (m->n_dof - nk_dof), s),
                                "cudaMemsetAsync");
     if (st) return st;
   }
   const int nz = int(m->plan.zero_cols.size());
   if (nz > 0) {
     const int blocks = int(std::min<int64_t>((int64_t(nz) * 32 + 255) / 256, 148 * 16));
-    zero_boundary_kernel<<<blocks, 256, 0, s>>>(m->d_col, m->d_plan.zero_cols, nz, m->L, R,
-                                                need_j ? d_vals : nullptr);
+    zero_boundary_kernel<<<blocks, 256, 0, s>>>(m->d_col, m->d_plan.zero_cols, nz, m->L, c.R, c.vals);
     fo_status st = cuda_status(cudaGetLastError(), "zero_boundary_kernel launch");
     if (st) return st;
-    ++launches;
+    ++c.launches;
   }
-  const bool n3 = m->p.glen_n == 3.0;
-  fo_status st;
+  return FO_OK;
+}
+
+fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1) {
+  if (p1 <= p0) return FO_OK;
+  fo_mesh m = c.m;
+  const bool need_j = c.vals != nullptr, n3 = m->p.glen_n == 3.0, tet = m->elem_type == FO_ELEM_TET3;
+  const int np = p1 - p0;
   // wedge R + J: the warp-specialised kernel unless the round-1 kernel is asked for
-  const bool ws = need_j && m->elem_type == FO_ELEM_WEDGE &&
-                  (m->scatter == FO_SCATTER_OWNER || m->scatter == FO_SCATTER_OWNER_WS);
+  const bool ws = need_j && !tet && (m->scatter == FO_SCATTER_OWNER || m->scatter == FO_SCATTER_OWNER_WS);
+  fo_status st;
   if (ws)
-    st = n3 ? launch_ws<true>(m, d_U, R, d_vals, s) : launch_ws<false>(m, d_U, R, d_vals, s);
+    st = n3 ? launch_ws<true>(m, c.U, c.R, c.vals, s, p0, np) : launch_ws<false>(m, c.U, c.R, c.vals, s, p0, np);
   else if (need_j)
-    st = m->elem_type == FO_ELEM_TET3
-             ? (n3 ? launch_patch<true, true, true>(m, d_U, R, d_vals, s) : launch_patch<true, false, true>(m, d_U, R, d_vals, s))
-             : (n3 ? launch_patch<true, true, false>(m, d_U, R, d_vals, s) : launch_patch<true, false, false>(m, d_U, R, d_vals, s));
+    st = tet ? (n3 ? launch_patch<true, true, true>(m, c.U, c.R, c.vals, s, p0, np)
+                   : launch_patch<true, false, true>(m, c.U, c.R, c.vals, s, p0, np))
+             : (n3 ? launch_patch<true, true, false>(m, c.U, c.R, c.vals, s, p0, np)
+                   : launch_patch<true, false, false>(m, c.U, c.R, c.vals, s, p0, np));
   else
-    st = m->elem_type == FO_ELEM_TET3
-             ? (n3 ? launch_patch<false, true, true>(m, d_U, R, nullptr, s) : launch_patch<false, false, true>(m, d_U, R, nullptr, s))
-             : (n3 ? launch_patch<false, true, false>(m, d_U, R, nullptr, s) : launch_patch<false, false, false>(m, d_U, R, nullptr, s));
+    st = tet ? (n3 ? launch_patch<false, true, true>(m, c.U, c.R, nullptr, s, p0, np)
+                   : launch_patch<false, false, true>(m, c.U, c.R, nullptr, s, p0, np))
+             : (n3 ? launch_patch<false, true, false>(m, c.U, c.R, nullptr, s, p0, np)
+                   : launch_patch<false, false, false>(m, c.U, c.R, nullptr, s, p0, np));
   if (st) return st;
-  ++launches;
-  const int nm = int(m->plan.multi.size());
-  if (nm > 0) {
-    const int n = nm * (m->L + 1);
-    multi_fixup_kernel<<<(n + 127) / 128, 128, 0, s>>>(m->d_plan.multi, nm, m->L, m->d_plan.partials, R,
-                                                       need_j ? d_vals : nullptr);
-    st = cuda_status(cudaGetLastError(), "multi_fixup_kernel launch");
-    if (st) return st;
-    ++launches;
-  }
-  m->last_launches = launches;
+  ++c.launches;
+  return FO_OK;
+}
+
+fo_status owner_multi(OwnerCall& c, cudaStream_t s, int r0, int r1) {
+  if (r1 <= r0) return FO_OK;
+  fo_mesh m = c.m;
+  const int n = (r1 - r0) * (m->L + 1);
+  multi_fixup_kernel<<<(n + 127) / 128, 128, 0, s>>>(m->d_plan.multi + r0, r1 - r0, m->L, m->d_plan.partials,
+                                                     c.R, c.vals);
+  fo_status st = cuda_status(cudaGetLastError(), "multi_fixup_kernel launch");
+  if (st) return st;
+  ++c.launches;
+  return FO_OK;
+}
+}  // namespace
+
+fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s) {
+  OwnerCall c;
+  fo_status st = owner_begin(c, m, d_U, d_R, d_vals);
+  if (!st) st = owner_prologue(c, s);
+  if (!st) st = owner_patches(c, s, 0, m->plan.n_patches);
+  if (!st) st = owner_multi(c, s, 0, int(m->plan.multi.size()));
+  if (st) return st;
+  m->last_launches = c.launches;
+  return FO_OK;
+}
+
+// Boundary-first assembly of a part mesh (fo_assemble_jacobian_halo): the
+// patches holding every ghost-touching triangle and the fix-up of the multi
+// columns they alone touch run on `side` (a higher-priority stream), the
+// interior patches on `s` at the same time; `ev_b` is recorded on `side` once
+// the ghost rows are final, so the halo sum can send them while the interior
+// patches are still running.  On return `s` has joined `side` for the
+// remaining fix-up; everything after it (lateral term, unpack-add) goes on s.
+fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
+                               cudaStream_t side, cudaEvent_t ev0, cudaEvent_t ev_b) {
+  OwnerCall c;
+  fo_status st = owner_begin(c, m, d_U, d_R, d_vals);
+  if (!st) st = owner_prologue(c, s);
+  if (!st) st = cuda_status(cudaEventRecord(ev0, s), "cudaEventRecord");
+  if (!st) st = cuda_status(cudaStreamWaitEvent(side, ev0, 0), "cudaStreamWaitEvent");
+  const int K = m->plan.n_bnd_patches, nmb = m->plan.n_multi_bnd;
+  if (!st) st = owner_patches(c, side, 0, K);
+  if (!st) st = owner_multi(c, side, 0, nmb);
+  if (!st) st = cuda_status(cudaEventRecord(ev_b, side), "cudaEventRecord");
+  if (!st) st = owner_patches(c, s, K, m->plan.n_patches);
+  if (!st) st = cuda_status(cudaStreamWaitEvent(s, ev_b, 0), "cudaStreamWaitEvent");
+  if (!st) st = owner_multi(c, s, nmb, int(m->plan.multi.size()));
+  if (st) return st;
+  m->last_launches = c.launches;
   return FO_OK;
 }
 
 }  // namespace fo
-
-#ifdef FO_TRACE
-extern "C" __attribute__((visibility("default"))) int fo_debug_trace(unsigned long long* host, long n) {
-  if (n > long(fo::kTraceMax) * fo::kTraceSlots) n = long(fo::kTraceMax) * fo::kTraceSlots;
-  return int(cudaMemcpyFromSymbol(host, fo::g_trace, size_t(n) * 8));
-}
-#endif

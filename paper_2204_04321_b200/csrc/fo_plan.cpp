@@ -233,6 +233,21 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
       }
     P.n_partials = nb;
   }
+  // part meshes: the leading patches holding the ghost-touching triangles, and
+  // the multi columns touched by those patches only (their fix-up can run
+  // before the interior patches are done), moved to the front of the list
+  for (int32_t p = 0; p < P.n_patches; ++p)
+    if (P.t_begin[size_t(p)] < m->n_bnd_tri) P.n_bnd_patches = p + 1;
+  if (P.n_bnd_patches > 0 && !P.multi.empty()) {
+    std::vector<int32_t> last(size_t(m->n_col), -1);
+    for (int32_t p = 0; p < P.n_patches; ++p)
+      for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci)
+        last[size_t(P.cols[size_t(ci)].c)] = p;
+    std::stable_partition(P.multi.begin(), P.multi.end(),
+                          [&](const MultiRec& r) { return last[size_t(r.c)] < P.n_bnd_patches; });
+    for (const MultiRec& r : P.multi)
+      if (last[size_t(r.c)] < P.n_bnd_patches) ++P.n_multi_bnd;
+  }
   // one 16-byte aligned blob per patch in the shared-memory layout of the
   // kernel (pairs | columns | contributions: the 16-byte pair records first,
   // so they stay 16-byte aligned), copied with one bulk copy

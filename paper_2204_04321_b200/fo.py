@@ -76,6 +76,7 @@ _SIGS = {
     "fo_halo_create_loopback": [P, P, I32, P],
     "fo_halo_import": [P, P, P],
     "fo_halo_sum": [P, P, P, P],
+    "fo_assemble_jacobian_halo": [P, P, P, P, P, P, P],
     "fo_halo_info": [P, P, P, P],
     "fo_halo_plan_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P],
     "fo_part_graph_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P, P],
@@ -255,6 +256,15 @@ class Halo:
 
     def sum(self, R=None, vals=None, stream=None):
         check(lib().fo_halo_sum(self.handle, _ptr(R), _ptr(vals), _stream_ptr(stream)), "fo_halo_sum")
+
+    def assemble(self, U, R, vals=None, stream=None):
+        """fo_assemble_jacobian_halo: assembly of the local mesh (R, and the
+        CSR values if vals is given) with the ghost-row sum overlapped; the
+        ghost U must be imported first.  R / vals are overwritten."""
+        g = self.mesh.graph() if vals is not None else None
+        check(lib().fo_assemble_jacobian_halo(self.mesh.handle, g.handle if g is not None else None, self.handle,
+                                              _ptr(U), _ptr(R), _ptr(vals), _stream_ptr(stream)),
+              "fo_assemble_jacobian_halo")
 
     def close(self):
         if self.handle:

@@ -1,6 +1,6 @@
 """NCCL halo check, one rank per GPU (torchrun --nproc-per-node N):
-fo_halo_create (NCCL) -> fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum,
-then the owned rows of every rank against the single-domain assembly on the
+fo_halo_create (NCCL) -> fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum
+(and fo_assemble_jacobian_halo, bit for bit the same owned rows), then the owned rows of every rank against the single-domain assembly on the
 same GPU (R <= 1e-12 max|R|, J <= 1e-11 row-scaled) and the imported ghost U
 bit for bit.  Used by tests/test_gpu_halo.py::test_nccl_halo_two_ranks (only on
 boxes with >= 2 GPUs).  Prints "halo_nccl_check OK" on rank 0.
@@ -35,7 +35,15 @@ def main():
     halo.import_(U)
     R, V = m.jacobian(U)
     halo.sum(R, V)
+    # fo_assemble_jacobian_halo (export overlapped with the interior patches):
+    # the owned rows bit for bit as the sequential call pair
+    Rf2, Vf2 = torch.full_like(R, float("nan")), torch.full_like(V, float("nan"))
+    halo.assemble(U, Rf2, Vf2)
     torch.cuda.synchronize()
+    no_ = m.n_owned_dofs
+    nv_ = int(m.graph().to_host()[0][no_])
+    assert Rf2[:no_].cpu().numpy().tobytes() == R[:no_].cpu().numpy().tobytes(), "fused R"
+    assert Vf2[:nv_].cpu().numpy().tobytes() == V[:nv_].cpu().numpy().tobytes(), "fused J"
     U, R, V = U.cpu().numpy(), R.cpu().numpy(), V.cpu().numpy()
     want = fp.U.reshape(fp.n_vert, L1, 2)[glob[nA:nA + nB]].reshape(-1)
     assert U[2 * nA * L1:2 * (nA + nB) * L1].tobytes() == want.tobytes(), "ghost U import"
