@@ -3,8 +3,10 @@
 
 Metric (BASELINE.json): "FO-Stokes Jacobian+residual assembly Melem/s per GPU,
 % HBM roofline, 1-8 GPU".  One step = one Total Fill of PAPER.md P:388:
-[ghost import of U] -> fo_assemble_jacobian (R and J in one pass) ->
-[ghost-row sum], on a synthetic extruded Greenland-like mesh with 10 layers:
+fo_assemble_jacobian (R and J in one pass) at N = 1; at N > 1
+fo_halo_import -> fo_assemble_jacobian_halo (assembly with the ghost-row sum
+overlapped; --halo sequential: fo_assemble_jacobian then fo_halo_sum), on a
+synthetic extruded Greenland-like mesh with 10 layers:
   N = 1: config C3 (1-10 km graded footprint sized to the paper's 479,930
          triangles, P:596), 4.8 M wedges;
   N > 1: config C4, the C3 recipe refined to N x 479,930 triangles, footprint
@@ -18,11 +20,13 @@ metric's "per GPU") and, at N > 1, the scaling efficiency of P:531-535 against
 the one-GPU time of the base mesh measured in the same run.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config auto|C3|C4|C5] [--loopback P]
+                    [--config auto|C3|C4|C5] [--loopback P] [--halo fused|sequential]
 
 --loopback P (N = 1): also time the P-part split of the workload on the one
-GPU through the library's halo path (fo_halo_import -> assemble every part ->
-fo_halo_sum, loopback transport): the multi-GPU code path end to end.
+GPU through the library's halo path (loopback transport), both the sequential
+(fo_halo_import -> fo_assemble_jacobian -> fo_halo_sum on every part) and the
+fused (fo_halo_import -> fo_assemble_jacobian_halo) step: the multi-GPU code
+path end to end.
 
 --impl reference runs the CPU oracle (oracle/, the serial C++ FE assembly the
 CUDA path is validated against) on the host cores, rank 0 only.
