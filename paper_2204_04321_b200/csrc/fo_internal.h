@@ -104,6 +104,11 @@ struct PatchPlan {
   // ghost column; multi records [0, n_multi_bnd) are touched by those patches only
   int32_t n_bnd_patches = 0;
   int32_t n_multi_bnd = 0;
+  // in-kernel zero fill (KA-ws, single launch): the LEAD patch of a boundary
+  // column (the first patch touching it) zero-fills it; zl[zl_ptr[p] ..
+  // zl_ptr[p+1]) are the columns patch p leads, wl[wl_ptr[p] .. wl_ptr[p+1])
+  // the lead patches p waits for before its first boundary RED
+  std::vector<int32_t> zl, zl_ptr, wl, wl_ptr;
 };
 
 struct DevPatch {
@@ -120,6 +125,11 @@ struct DevPatch {
   int32_t* nedge = nullptr;          // [n_patches]
   MultiRec* multi = nullptr;
   double* partials = nullptr;        // [n_partials][L+1][kPartialStride]
+  int32_t* zl = nullptr;
+  int32_t* zl_ptr = nullptr;
+  int32_t* wl = nullptr;
+  int32_t* wl_ptr = nullptr;
+  int32_t* flags = nullptr;          // [n_patches + 1]: zero-fill done per patch; [n_patches] = patch ticket
 };
 
 }  // namespace fo

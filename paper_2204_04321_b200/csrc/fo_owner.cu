@@ -40,6 +40,17 @@ struct PlanView {
   const int64_t* __restrict__ blob_off;
   double* partials;   // multi columns' partial blocks (fo_plan.cpp)
   int p_off;          // patch of block 0 (a launch covers patches p_off .. p_off + gridDim.x - 1)
+  // KA-ws in-kernel zero fill (inkz != 0, single launch over all patches):
+  // patches are taken in ticket order (flags[n_patches]), each zero-fills the
+  // boundary columns it leads (zl), raises flags[p], and waits for the flags
+  // of the leads of its other boundary columns (wl)
+  const int32_t* __restrict__ zl;
+  const int32_t* __restrict__ zl_ptr;
+  const int32_t* __restrict__ wl;
+  const int32_t* __restrict__ wl_ptr;
+  int32_t* flags;
+  int inkz;
+  int n_patches;
 };
 
 
@@ -426,7 +437,7 @@ constexpr int kWsThreads = 256;
 // (208 / 48 spilled the scatter's addresses: C3 1.471 vs 1.403 ms; 192 / 64: 1.496)
 constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;
 constexpr int kPlanOffsetWS = ((kD + kO) * TP * 8 + 15) / 16 * 16;
-constexpr int kBarEmpty = 1, kBarFull = 2, kBarElem = 3;
+constexpr int kBarEmpty = 1, kBarFull = 2, kBarElem = 3, kBarScat = 4;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -445,7 +456,13 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   double* const O = smem + kD * TP;    // [kO][TP]
   __shared__ uint64_t plan_bar;
   __shared__ uint32_t tmem_base;
-  const int p = pv.p_off + int(blockIdx.x);
+  __shared__ int ticket;
+  if (pv.inkz && threadIdx.x == 0) ticket = atomicAdd(pv.flags + pv.n_patches, 1);
+  __syncthreads();
+  // with the in-kernel zero fill a CTA's patch is its ticket: a lead patch
+  // (lower ticket) belongs to a CTA that is already running, so waiting for it
+  // cannot deadlock
+  const int p = pv.inkz ? ticket : pv.p_off + int(blockIdx.x);
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   SmemPlan sp;
   char* const base = reinterpret_cast<char*>(smem) + kPlanOffsetWS;
@@ -537,6 +554,38 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     // ---------------- WG1: scatter (phase B) ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsB));
     const int tb = int(threadIdx.x) - 128;
+    if (pv.inkz) {
+      // while the element warps compute layer 0: zero-fill the boundary
+      // columns this patch leads (a warp per column), publish, then wait for
+      // the leads of the other boundary columns before the first RED
+      const int z0 = __ldg(pv.zl_ptr + p), z1 = __ldg(pv.zl_ptr + p + 1);
+      const int lane = tb & 31;
+      for (int i = z0 + (tb >> 5); i < z1; i += 4) {
+        const int c = __ldg(pv.zl + i);
+        for (int j = lane; j < L + 1; j += 32)
+          *reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)) = make_double2(0.0, 0.0);
+        const long long csn = __double_as_longlong(__ldg(reinterpret_cast<const double*>(col + c) + 5));
+        double2* v = reinterpret_cast<double2*>(vals + (csn >> 8));
+        const int64_t len2 = int64_t(2 * (csn & 255)) * (3 * L + 1);
+        for (int64_t j = lane; j < len2; j += 32) v[j] = make_double2(0.0, 0.0);
+      }
+      named_sync(kBarScat, 128);
+      if (tb == 0) {
+        __threadfence();   // the scatter warps' zero stores (ordered by the barrier) before the flag
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(pv.flags + p), "r"(1) : "memory");
+      }
+      const int w0 = __ldg(pv.wl_ptr + p), w1 = __ldg(pv.wl_ptr + p + 1);
+      for (int i = w0 + tb; i < w1; i += 128) {
+        const int32_t* f = pv.flags + __ldg(pv.wl + i);
+        int v = 0;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          if (v) break;
+          __nanosleep(64);
+        }
+      }
+      named_sync(kBarScat, 128);
+    }
     bulk_wait(&plan_bar);
     named_arrive(kBarEmpty, kWsThreads);   // D / O start free
     for (int kk = 0; kk <= L; ++kk) {
@@ -613,13 +662,15 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
 static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
 template <bool N3>
-static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np) {
+static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np,
+                           bool inkz) {
   const size_t sm = size_t(kPlanOffsetWS) + kPlanBytes;
   fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sm)), "cudaFuncSetAttribute");
   if (st) return st;
-  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
-              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials, p0};
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
+              m->d_plan.blob_off, m->d_plan.partials, p0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
+              m->d_plan.wl_ptr, m->d_plan.flags, inkz ? 1 : 0, m->plan.n_patches};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
@@ -647,8 +698,9 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
                                "cudaFuncSetAttribute");
     if (st) return st;
   }
-  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr,  m->d_plan.pair_ptr, m->d_plan.nedge,
-              m->d_plan.blob,    m->d_plan.blob_off, m->d_plan.partials, p0};
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
+              m->d_plan.blob_off, m->d_plan.partials, p0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
+              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
@@ -693,8 +745,22 @@ fo_status owner_begin(OwnerCall& c, fo_mesh m, const double* d_U, double* d_R, d
   return FO_OK;
 }
 
-fo_status owner_prologue(OwnerCall& c, cudaStream_t s) {
+// the wedge R + J path runs the warp-specialised kernel unless the round-1 kernel is asked for
+bool uses_ws(const OwnerCall& c) {
+  return c.vals != nullptr && c.m->elem_type != FO_ELEM_TET3 &&
+         (c.m->scatter == FO_SCATTER_OWNER || c.m->scatter == FO_SCATTER_OWNER_WS);
+}
+
+// inkz: the warp-specialised kernel zero-fills the boundary columns itself
+// (single launch over all patches): reset its flags and ticket instead of
+// launching zero_boundary_kernel
+fo_status owner_prologue(OwnerCall& c, cudaStream_t s, bool inkz = false) {
   fo_mesh m = c.m;
+  if (inkz) {
+    fo_status st = cuda_status(cudaMemsetAsync(m->d_plan.flags, 0, sizeof(int32_t) * (m->plan.n_patches + 1), s),
+                               "cudaMemsetAsync");
+    if (st) return st;
+  }
   const int64_t nk_dof = 2 * (m->nA + m->nB) * (m->L + 1);
   if (nk_dof < m->n_dof) {   // column-only (class C) DOFs: residual 0
     fo_status st = cuda_status(cudaMemsetAsync(c.R + nk_dof, 0, sizeof(double) * (m->n_dof - nk_dof), s),
@@ -702,7 +768,7 @@ fo_status owner_prologue(OwnerCall& c, cudaStream_t s) {
     if (st) return st;
   }
   const int nz = int(m->plan.zero_cols.size());
-  if (nz > 0) {
+  if (nz > 0 && !inkz) {
     const int blocks = int(std::min<int64_t>((int64_t(nz) * 32 + 255) / 256, 148 * 16));
     zero_boundary_kernel<<<blocks, 256, 0, s>>>(m->d_col, m->d_plan.zero_cols, nz, m->L, c.R, c.vals);
     fo_status st = cuda_status(cudaGetLastError(), "zero_boundary_kernel launch");
@@ -712,16 +778,15 @@ fo_status owner_prologue(OwnerCall& c, cudaStream_t s) {
   return FO_OK;
 }
 
-fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1) {
+fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1, bool inkz = false) {
   if (p1 <= p0) return FO_OK;
   fo_mesh m = c.m;
   const bool need_j = c.vals != nullptr, n3 = m->p.glen_n == 3.0, tet = m->elem_type == FO_ELEM_TET3;
   const int np = p1 - p0;
-  // wedge R + J: the warp-specialised kernel unless the round-1 kernel is asked for
-  const bool ws = need_j && !tet && (m->scatter == FO_SCATTER_OWNER || m->scatter == FO_SCATTER_OWNER_WS);
   fo_status st;
-  if (ws)
-    st = n3 ? launch_ws<true>(m, c.U, c.R, c.vals, s, p0, np) : launch_ws<false>(m, c.U, c.R, c.vals, s, p0, np);
+  if (uses_ws(c))
+    st = n3 ? launch_ws<true>(m, c.U, c.R, c.vals, s, p0, np, inkz)
+            : launch_ws<false>(m, c.U, c.R, c.vals, s, p0, np, inkz);
   else if (need_j)
     st = tet ? (n3 ? launch_patch<true, true, true>(m, c.U, c.R, c.vals, s, p0, np)
                    : launch_patch<true, false, true>(m, c.U, c.R, c.vals, s, p0, np))
@@ -753,8 +818,10 @@ fo_status owner_multi(OwnerCall& c, cudaStream_t s, int r0, int r1) {
 fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s) {
   OwnerCall c;
   fo_status st = owner_begin(c, m, d_U, d_R, d_vals);
-  if (!st) st = owner_prologue(c, s);
-  if (!st) st = owner_patches(c, s, 0, m->plan.n_patches);
+  // one launch over all patches: the warp-specialised kernel zero-fills in-kernel
+  const bool inkz = !st && uses_ws(c);
+  if (!st) st = owner_prologue(c, s, inkz);
+  if (!st) st = owner_patches(c, s, 0, m->plan.n_patches, inkz);
   if (!st) st = owner_multi(c, s, 0, int(m->plan.multi.size()));
   if (st) return st;
   m->last_launches = c.launches;

@@ -145,7 +145,7 @@ size_t plan_bytes(const PatchBuild& B) {
 void free_patch_plan(fo_mesh m) {
   DevPatch& d = m->d_plan;
   void* ptrs[] = {d.t_begin, d.col_ptr, d.pair_ptr, d.contrib_ptr, d.cols, d.pairs, d.contrib, d.zero_cols,
-                  d.blob, d.blob_off, d.nedge, d.multi, d.partials};
+                  d.blob, d.blob_off, d.nedge, d.multi, d.partials, d.zl, d.zl_ptr, d.wl, d.wl_ptr, d.flags};
   for (void* q : ptrs) cudaFree(q);
   d = DevPatch();
   m->plan = PatchPlan();
@@ -206,6 +206,30 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
   P.n_patches = int32_t(P.t_begin.size() - 1);
   for (int64_t c = 0; c < nk; ++c)
     if (boundary[size_t(c)]) P.zero_cols.push_back(int32_t(c));
+  {   // lead patch of every boundary column, its zero list and the wait lists
+    std::vector<int32_t> lead(size_t(m->n_col), -1);
+    for (int32_t p = 0; p < P.n_patches; ++p)
+      for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci)
+        if (lead[size_t(P.cols[size_t(ci)].c)] < 0) lead[size_t(P.cols[size_t(ci)].c)] = p;
+    P.zl_ptr.assign(size_t(P.n_patches) + 1, 0);
+    for (int32_t c : P.zero_cols) P.zl_ptr[size_t(lead[size_t(c)]) + 1]++;
+    for (int32_t p = 0; p < P.n_patches; ++p) P.zl_ptr[size_t(p) + 1] += P.zl_ptr[size_t(p)];
+    P.zl.assign(P.zero_cols.size(), 0);
+    std::vector<int32_t> fill(P.zl_ptr.begin(), P.zl_ptr.end() - 1);
+    for (int32_t c : P.zero_cols) P.zl[size_t(fill[size_t(lead[size_t(c)])]++)] = c;
+    P.wl_ptr.assign(1, 0);
+    for (int32_t p = 0; p < P.n_patches; ++p) {
+      std::vector<int32_t> w;
+      for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci) {
+        const int32_t c = P.cols[size_t(ci)].c;
+        if (boundary[size_t(c)] && lead[size_t(c)] != p) w.push_back(lead[size_t(c)]);
+      }
+      std::sort(w.begin(), w.end());
+      w.erase(std::unique(w.begin(), w.end()), w.end());
+      P.wl.insert(P.wl.end(), w.begin(), w.end());
+      P.wl_ptr.push_back(int32_t(P.wl.size()));
+    }
+  }
   // MULTI columns: touched by >= 3 patches; partial block b = base + rank
   // (rank = order of the patch among the column's patches)
   {
@@ -275,6 +299,13 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
   if (!st) st = upload_vec(&m->d_plan.nedge, P.nedge);
   if (!st) st = upload_vec(&m->d_plan.zero_cols, P.zero_cols);
   if (!st) st = upload_vec(&m->d_plan.multi, P.multi);
+  if (!st) st = upload_vec(&m->d_plan.zl, P.zl);
+  if (!st) st = upload_vec(&m->d_plan.zl_ptr, P.zl_ptr);
+  if (!st) st = upload_vec(&m->d_plan.wl, P.wl);
+  if (!st) st = upload_vec(&m->d_plan.wl_ptr, P.wl_ptr);
+  if (!st)
+    st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.flags), sizeof(int32_t) * (P.n_patches + 1)),
+                     "cudaMalloc");
   if (!st && P.n_partials > 0)
     st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.partials),
                                 sizeof(double) * kPartialStride * size_t(m->L + 1) * size_t(P.n_partials)),
@@ -357,6 +388,29 @@ fo_status plan_check(const fo_mesh m, int64_t* stats) {
     }
     int rs = rstore[size_t(c)] + (multi[size_t(c)] ? 1 : 0), rr = rred[size_t(c)];
     if (!((rs == 1 && rr == 0) || (rs == 0 && rr >= 1 && zeroed[size_t(c)]))) ++bad_slot;
+  }
+  // in-kernel zero fill of KA-ws: every zero-filled column is in the zero list
+  // of exactly one patch -- the first patch holding it -- and every later
+  // patch holding it waits for that patch
+  {
+    std::vector<int32_t> lead_of(size_t(m->n_col), -1);
+    for (int32_t p = 0; p < P.n_patches; ++p)
+      for (int32_t i = P.zl_ptr[size_t(p)]; i < P.zl_ptr[size_t(p) + 1]; ++i) {
+        if (lead_of[size_t(P.zl[size_t(i)])] >= 0) ++bad_slot;
+        lead_of[size_t(P.zl[size_t(i)])] = p;
+      }
+    for (int32_t c : P.zero_cols)
+      if (lead_of[size_t(c)] < 0) ++bad_slot;
+    for (int32_t p = 0; p < P.n_patches; ++p) {
+      const int32_t* w0 = P.wl.data() + P.wl_ptr[size_t(p)];
+      const int32_t* w1 = P.wl.data() + P.wl_ptr[size_t(p) + 1];
+      for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci) {
+        const int32_t c = P.cols[size_t(ci)].c, l = lead_of[size_t(c)];
+        if (!zeroed[size_t(c)]) continue;
+        if (l > p) ++bad_slot;   // the lead is the FIRST patch holding the column
+        if (l != p && !std::binary_search(w0, w1, l)) ++bad_slot;
+      }
+    }
   }
   stats[0] = P.n_patches;
   stats[1] = int64_t(P.pairs.size());
