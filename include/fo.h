@@ -241,8 +241,11 @@ FO_API fo_status fo_set_lateral(fo_mesh m, int enable);
  * FO_SCATTER_OWNER    column-patch owner-computes kernel: every CSR value of an
  *                     interior column written exactly once with plain stores
  *                     (deterministic); for wedges the warp-specialised kernel
- *                     (element warpgroup with TMEM scratch + scatter warpgroup)
- * FO_SCATTER_ATOMIC   one thread per wedge, fp64 atomics into zeroed outputs
+ *                     (element warpgroup with TMEM scratch + scatter warpgroup);
+ *                     for hexahedra the quad-patch kernel (KH-patch)
+ * FO_SCATTER_ATOMIC   one thread per wedge, fp64 atomics into zeroed outputs;
+ *                     hexahedra: one thread per hexahedron, coloured
+ *                     read-modify-write into zeroed outputs
  * FO_SCATTER_OWNER_WS the warp-specialised kernel explicitly (wedges, R + J)
  * FO_SCATTER_OWNER_1WG the round-1 single-warpgroup patch kernel (element and
  *                     scatter phases alternate in the same threads). */

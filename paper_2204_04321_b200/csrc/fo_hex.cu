@@ -26,6 +26,7 @@
 
 #include "fo_internal.h"
 #include "fo_kernels.cuh"
+#include "fo_patch.cuh"
 
 namespace fo {
 
@@ -104,6 +105,47 @@ __device__ __forceinline__ void hex_visc(const HexIn& h, const double G[8][3], d
   for (int i = 0; i < 8; ++i) {
     g[2 * i] = fma(e1x, G[i][0], fma(exy, G[i][1], exz * G[i][2]));
     g[2 * i + 1] = fma(exy, G[i][0], fma(e2y, G[i][1], eyz * G[i][2]));
+  }
+}
+
+// basal Robin term on the bilinear bottom face (readings L6-L8):
+// 2 x 2 Gauss points with the true 3D area element; adds into the bottom
+// residual r[0..8) and, NEED_J, the (bottom, bottom) block bb (packed p <= p2)
+template <bool NEED_J>
+__device__ __forceinline__ void hex_basal(const HexIn& h, double (&r)[16], double (&bb)[36]) {
+  constexpr double gz = 0.57735026918962576451;
+  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+#pragma unroll
+  for (int qp = 0; qp < 4; ++qp) {
+    const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz;
+    double Q[4], tx0 = 0, tx1 = 0, tx2 = 0, ty0 = 0, ty1 = 0, ty2 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      Q[j] = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+      const double dxi = 0.25 * cxi[j] * (1.0 + ceta[j] * eta), deta = 0.25 * ceta[j] * (1.0 + cxi[j] * xi);
+      tx0 = fma(dxi, h.X[j], tx0); tx1 = fma(dxi, h.Y[j], tx1); tx2 = fma(dxi, h.Zb[j], tx2);
+      ty0 = fma(deta, h.X[j], ty0); ty1 = fma(deta, h.Y[j], ty1); ty2 = fma(deta, h.Zb[j], ty2);
+    }
+    const double cx = tx1 * ty2 - tx2 * ty1, cy = tx2 * ty0 - tx0 * ty2, cz = tx0 * ty1 - tx1 * ty0;
+    const double w = sqrt(cx * cx + cy * cy + cz * cz);
+    const double bq = w * (Q[0] * h.B[0] + Q[1] * h.B[1] + Q[2] * h.B[2] + Q[3] * h.B[3]);
+    const double u = Q[0] * h.Uu[0] + Q[1] * h.Uu[1] + Q[2] * h.Uu[2] + Q[3] * h.Uu[3];
+    const double v = Q[0] * h.Uv[0] + Q[1] * h.Uv[1] + Q[2] * h.Uv[2] + Q[3] * h.Uv[3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      r[2 * j] += bq * Q[j] * u;
+      r[2 * j + 1] += bq * Q[j] * v;
+    }
+    if (NEED_J) {
+      int e = 0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int p2 = p; p2 < 8; ++p2) {
+          if ((p & 1) == (p2 & 1)) bb[e] += bq * Q[p >> 1] * Q[p2 >> 1];
+          ++e;
+        }
+    }
   }
 }
 
@@ -227,42 +269,7 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
         for (int p2 = p; p2 < 8; ++p2) bb[e++] += hex_jentry(G, g, c, d, p, p2);
     }
   }
-  if (k == 0) {   // basal Robin term on the bilinear bottom face
-    constexpr double gz = 0.57735026918962576451;
-    const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
-#pragma unroll
-    for (int qp = 0; qp < 4; ++qp) {
-      const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz;
-      double Q[4], tx0 = 0, tx1 = 0, tx2 = 0, ty0 = 0, ty1 = 0, ty2 = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        Q[j] = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
-        const double dxi = 0.25 * cxi[j] * (1.0 + ceta[j] * eta), deta = 0.25 * ceta[j] * (1.0 + cxi[j] * xi);
-        tx0 = fma(dxi, h.X[j], tx0); tx1 = fma(dxi, h.Y[j], tx1); tx2 = fma(dxi, h.Zb[j], tx2);
-        ty0 = fma(deta, h.X[j], ty0); ty1 = fma(deta, h.Y[j], ty1); ty2 = fma(deta, h.Zb[j], ty2);
-      }
-      const double cx = tx1 * ty2 - tx2 * ty1, cy = tx2 * ty0 - tx0 * ty2, cz = tx0 * ty1 - tx1 * ty0;
-      const double w = sqrt(cx * cx + cy * cy + cz * cz);
-      const double bq = w * (Q[0] * h.B[0] + Q[1] * h.B[1] + Q[2] * h.B[2] + Q[3] * h.B[3]);
-      const double u = Q[0] * h.Uu[0] + Q[1] * h.Uu[1] + Q[2] * h.Uu[2] + Q[3] * h.Uu[3];
-      const double v = Q[0] * h.Uv[0] + Q[1] * h.Uv[1] + Q[2] * h.Uv[2] + Q[3] * h.Uv[3];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        r[2 * j] += bq * Q[j] * u;
-        r[2 * j + 1] += bq * Q[j] * v;
-      }
-      if (NEED_J) {
-        int e = 0;
-#pragma unroll
-        for (int p = 0; p < 8; ++p)
-#pragma unroll
-          for (int p2 = p; p2 < 8; ++p2) {
-            if ((p & 1) == (p2 & 1)) bb[e] += bq * Q[p >> 1] * Q[p2 >> 1];
-            ++e;
-          }
-      }
-    }
-  }
+  if (k == 0) hex_basal<NEED_J>(h, r, bb);
   rmw_batch<8>([&](int i, double2*& p, double& v0, double& v1) {
     p = reinterpret_cast<double2*>(R) + int64_t(qr.v[i & 3]) * (L + 1) + k + (i >> 2);
     v0 = r[2 * i];
@@ -339,6 +346,300 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
   }
 }
 
+// One point's contribution c H - d g g^T to a block of the 16 x 16 element
+// matrix, with the row node's gradient prescaled once by the viscosity factor
+// (uu: (2 c Gx, c Gy / 2, c Gz / 2) . G', vv: (c Gx / 2, 2 c Gy, c Gz / 2) . G',
+// uv: c Gx Gy' + (c Gy / 2) Gx', vu: (c Gx / 2) Gy' + c Gy Gx', H of SURVEY.md
+// App. A.3): 3-4 FMA per entry instead of hex_jentry's products per entry.
+// BLK 0: (bottom, bottom) packed p <= p2 (36); 1: (bottom, top) [8 p + p2] (64);
+// 2: (top, top) packed (36).
+template <int BLK>
+__device__ __forceinline__ void hex_accum(const double G[8][3], const double g[16], double c, double d,
+                                          double* acc) {
+  constexpr int r0 = BLK == 2 ? 4 : 0, c0 = BLK == 0 ? 0 : 4;
+#pragma unroll
+  for (int i = r0; i < r0 + 4; ++i) {
+    const double cx = c * G[i][0], cy = c * G[i][1], cz = c * G[i][2];
+    const double ax = 2.0 * cx, ay = 0.5 * cy, az = 0.5 * cz, bx = 0.5 * cx, by = 2.0 * cy;
+    const double du = -d * g[2 * i], dv = -d * g[2 * i + 1];
+#pragma unroll
+    for (int i2 = c0; i2 < c0 + 4; ++i2) {
+      if (BLK != 1 && i2 < i) continue;
+      const double gx = G[i2][0], gy = G[i2][1], gz = G[i2][2];
+      const double uu = fma(du, g[2 * i2], fma(az, gz, fma(ay, gy, ax * gx)));
+      const double uv = fma(du, g[2 * i2 + 1], fma(ay, gx, cx * gy));
+      const double vv = fma(dv, g[2 * i2 + 1], fma(az, gz, fma(by, gy, bx * gx)));
+      const int p = 2 * (i - r0), p2 = 2 * (i2 - c0);
+      if (BLK == 1) {
+        const double vu = fma(dv, g[2 * i2], fma(cy, gx, bx * gy));
+        acc[8 * p + p2] += uu;
+        acc[8 * p + p2 + 1] += uv;
+        acc[8 * (p + 1) + p2] += vu;
+        acc[8 * (p + 1) + p2 + 1] += vv;
+      } else {
+        auto sym = [](int a, int b) { return a * 8 - (a * (a - 1)) / 2 + (b - a); };
+        acc[sym(p, p2)] += uu;
+        acc[sym(p, p2 + 1)] += uv;
+        acc[sym(p + 1, p2 + 1)] += vv;
+        if (i2 != i) acc[sym(p + 1, p2)] += fma(dv, g[2 * i2], fma(cy, gx, bx * gy));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KH-patch: owner-computes hexahedral assembly (DESIGN.md "Hexahedral
+// variant").  The wedge path's patch scheme on a quadrilateral footprint: one
+// CTA = <= kPatchQuads consecutive (Hilbert-ordered) quads, one thread per quad
+// column, layers k = 0..L-1.  Per layer the thread evaluates hexahedron (q, k)
+// in the three passes of hex_kernel and publishes into shared memory: the
+// (bottom, bottom) block and the bottom residual are ADDED to D (which holds
+// the (top, top) block + top residual of hexahedron (q, k-1): the vertical
+// merge of level k), the (bottom, top) block is STORED to O, the (top, top)
+// block + top residual stay in registers (held) and become D after phase B.
+// Phase B: one thread per (column, slot) pair of the patch gathers its
+// contributions (plan contribution lists, CodeBits<4>) and writes the CSR
+// values and R exactly like the wedge scatter (interior columns: plain stores;
+// boundary: RED onto the zero fill; multi columns: partial blocks + fix-up).
+constexpr int TPQ = kPatchStrideQ;   // SoA row stride of D / O (odd)
+using CBQ = CodeBits<4>;
+// D entry of (bottom dof p, bottom dof p2), p <= p2: 2x2 node blocks
+__host__ __device__ constexpr int dmap4(int p, int p2) {
+  return (p >> 1) == (p2 >> 1)
+             ? 24 + 3 * (p >> 1) + (p & 1) + (p2 & 1)
+             : 4 * ((p >> 1) * (7 - (p >> 1)) / 2 + ((p2 >> 1) - (p >> 1) - 1)) + 2 * (p & 1) + (p2 & 1);
+}
+constexpr int kHexDR = 36;   // residual entries of D: 36 + 2 j + a
+constexpr int kPlanOffsetQ = (kHexDE + kHexOE) * TPQ * 8 / 16 * 16 + 16;
+constexpr int kPlanOffsetQR = kHexDE * TPQ * 8 / 16 * 16 + 16;
+
+template <bool UP, bool FIRST>
+__device__ __forceinline__ void gather2q(uint2 c2, const double* D, const double* O, PairSums& s) {
+  constexpr unsigned mt = (1u << CBQ::kTl) - 1, md = (1u << CBQ::kDb) - 1, mo = (1u << CBQ::kOw) - 1;
+  const int tla = int(c2.x & mt), tlb = int(c2.y & mt);
+  const int pata = int((c2.x >> CBQ::kPat) & 3), patb = int((c2.y >> CBQ::kPat) & 3);
+  const int saa = pata == 1 ? 2 * TPQ : TPQ, sba = pata == 2 ? 2 * TPQ : TPQ;
+  const int sab = patb == 1 ? 2 * TPQ : TPQ, sbb = patb == 2 ? 2 * TPQ : TPQ;
+  const double* Da = D + int((c2.x >> CBQ::kTl) & md) * TPQ + tla;
+  const double* Db = D + int((c2.y >> CBQ::kTl) & md) * TPQ + tlb;
+  if (FIRST) {
+    s.dg[0] = Da[0] + Db[0];
+    s.dg[1] = Da[sba] + Db[sbb];
+    s.dg[2] = Da[saa] + Db[sab];
+    s.dg[3] = Da[saa + sba] + Db[sab + sbb];
+  } else {
+    s.dg[0] = (s.dg[0] + Da[0]) + Db[0];
+    s.dg[1] = (s.dg[1] + Da[sba]) + Db[sbb];
+    s.dg[2] = (s.dg[2] + Da[saa]) + Db[sab];
+    s.dg[3] = (s.dg[3] + Da[saa + sba]) + Db[sab + sbb];
+  }
+  if (UP) {
+    const double* Oua = O + int((c2.x >> CBQ::kO) & mo) * TPQ + tla;
+    const double* Ona = O + int((c2.x >> CBQ::kOt) & mo) * TPQ + tla;
+    const double* Oub = O + int((c2.y >> CBQ::kO) & mo) * TPQ + tlb;
+    const double* Onb = O + int((c2.y >> CBQ::kOt) & mo) * TPQ + tlb;
+    constexpr int ou[4] = {0, TPQ, 8 * TPQ, 9 * TPQ}, on[4] = {0, 8 * TPQ, TPQ, 9 * TPQ};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (FIRST) {
+        s.up[i] = Oua[ou[i]] + Oub[ou[i]];
+        s.nx[i] = Ona[on[i]] + Onb[on[i]];
+      } else {
+        s.up[i] = (s.up[i] + Oua[ou[i]]) + Oub[ou[i]];
+        s.nx[i] = (s.nx[i] + Ona[on[i]]) + Onb[on[i]];
+      }
+    }
+  }
+}
+
+template <bool UP>
+__device__ __forceinline__ void phase_bq_j(const SmemPlan& sp, int kk, int L, const double* D, const double* O,
+                                           double* __restrict__ vals, double* __restrict__ partials, int tid,
+                                           int nthr) {
+  for (int pi = tid; pi < sp.npairs; pi += nthr) {
+    const PlanPair pp = sp.pairs[pi];
+    PairSums s;
+    const uint32_t* cp = sp.contrib + pp.off - 2;
+    gather2q<UP, true>(make_uint2(pp.c0, pp.c1), D, O, s);
+    for (int e = 2; e < pp.cnt; e += 2) gather2q<UP, false>(*reinterpret_cast<const uint2*>(cp + e), D, O, s);
+    emit<UP>(pp, sp.cols[pp.col], s, kk, L, vals, partials);
+  }
+}
+
+__device__ __forceinline__ void phase_bq_r(const SmemPlan& sp, int kk, int L, const double* Dr,
+                                           double* __restrict__ R, double* __restrict__ partials, int tid,
+                                           int nthr) {
+  constexpr unsigned mt = (1u << CBQ::kTl) - 1;
+  for (int ci = tid; ci < sp.ncols; ci += nthr) {
+    const PlanCol& pc = sp.cols[ci];
+    double r0 = 0.0, r1 = 0.0;
+    for (int e = pc.self_off; e < pc.self_off + pc.self_cnt; e += 2) {
+      const uint2 c2 = *reinterpret_cast<const uint2*>(sp.contrib + e);
+      const double* Da = Dr + 2 * int((c2.x >> CBQ::kJ) & 3) * TPQ + int(c2.x & mt);
+      const double* Db = Dr + 2 * int((c2.y >> CBQ::kJ) & 3) * TPQ + int(c2.y & mt);
+      r0 += Da[0];
+      r1 += Da[TPQ];
+      r0 += Db[0];
+      r1 += Db[TPQ];
+    }
+    if ((pc.info >> 30) & 1)
+      *reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride + 12) =
+          make_double2(r0, r1);
+    else
+      put2(R + 2 * (int64_t(pc.c) * (L + 1) + kk), r0, r1, (pc.info >> 8) & 1);
+  }
+}
+
+template <bool NEED_J, bool N3>
+__global__ void __launch_bounds__(kPatchQuads, kHexCtasPerSm)
+kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads,
+                const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp, PlanView pv,
+                const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
+  extern __shared__ __align__(16) double smem[];
+  double* const D = smem;                  // [kHexDE][TPQ]
+  double* const O = smem + kHexDE * TPQ;   // [kHexOE][TPQ] (R + J)
+  const int p = int(blockIdx.x);
+  const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
+  __shared__ uint64_t plan_bar;
+  SmemPlan sp;
+  {
+    const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
+    const int q0 = __ldg(pv.pair_ptr + p), q1 = __ldg(pv.pair_ptr + p + 1);
+    const int64_t b0 = __ldg(pv.blob_off + p), b1 = __ldg(pv.blob_off + p + 1);
+    char* base = reinterpret_cast<char*>(smem) + (NEED_J ? kPlanOffsetQ : kPlanOffsetQR);
+    sp.pairs = reinterpret_cast<const PlanPair*>(base);
+    sp.cols = reinterpret_cast<const PlanCol*>(base + (q1 - q0) * sizeof(PlanPair));
+    sp.contrib = reinterpret_cast<const uint32_t*>(base + (c1 - c0) * sizeof(PlanCol) + (q1 - q0) * sizeof(PlanPair));
+    sp.ncols = c1 - c0; sp.npairs = q1 - q0;
+    sp.nedge = __ldg(pv.nedge + p);
+    if (threadIdx.x == 0) bulk_init(&plan_bar);
+    __syncthreads();
+    if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
+  }
+  const int L = kp.L;
+  const int tl = threadIdx.x;
+  const bool active = tl < nt;
+  const int qi = t0 + (active ? tl : 0);
+  const QuadRec qr = quads[qi];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < kHexDE; ++i) D[i * TPQ + tl] = 0.0;
+  }
+  // quad slot kPatchQuads: the zero column the plan's pad entries read
+  for (int i = threadIdx.x; i < kHexDE; i += blockDim.x) D[i * TPQ + kPatchQuads] = 0.0;
+  if (NEED_J)
+    for (int i = threadIdx.x; i < kHexOE; i += blockDim.x) O[i * TPQ + kPatchQuads] = 0.0;
+  double held[kHexDE];
+  for (int k = 0; k < L; ++k) {
+    if (active) {
+      HexIn h;
+      const double s0 = __ldg(sigma + k), s1 = __ldg(sigma + k + 1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const ColRec c = col[qr.v[j]];
+        h.X[j] = c.x;
+        h.Y[j] = c.y;
+        h.Zb[j] = fma(s0, c.H, c.base);
+        h.Zt[j] = fma(s1, c.H, c.base);
+        h.S[j] = c.base + c.H;
+        h.B[j] = c.beta;
+        const int64_t node = int64_t(qr.v[j]) * (L + 1) + k;
+        const double2 ub = __ldg(reinterpret_cast<const double2*>(U) + node);
+        const double2 ut = __ldg(reinterpret_cast<const double2*>(U) + node + 1);
+        h.Uu[j] = ub.x; h.Uv[j] = ub.y; h.Uu[j + 4] = ut.x; h.Uv[j + 4] = ut.y;
+      }
+      h.Afac = wedge_afac(kp, Aw, qi, k);
+      // ---- pass 1: residual, (bottom, bottom) block, basal term -> D (+=), top residual -> held
+      {
+        double r[16], bb[36];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 36; ++i) bb[i] = 0.0;
+#pragma unroll 1
+        for (int qp = 0; qp < 8; ++qp) {
+          double N[8], G[8][3], g[16], c, d;
+          const double W = hex_point(h, qp, N, G);
+          hex_visc<N3>(h, G, W, kp, g, c, d);
+          double sx = 0, sy = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) { sx = fma(h.S[i & 3], G[i][0], sx); sy = fma(h.S[i & 3], G[i][1], sy); }
+          const double bw = W * kp.rg;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            r[2 * i] += fma(c, g[2 * i], bw * sx * N[i]);
+            r[2 * i + 1] += fma(c, g[2 * i + 1], bw * sy * N[i]);
+          }
+          if (NEED_J) hex_accum<0>(G, g, c, d, bb);
+        }
+        if (k == 0) hex_basal<NEED_J>(h, r, bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) D[(kHexDR + i) * TPQ + tl] += r[i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) held[kHexDR + i] = r[8 + i];
+        if (NEED_J) {
+          int e = 0;
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp)
+#pragma unroll
+            for (int p2 = pp; p2 < 8; ++p2) { D[dmap4(pp, p2) * TPQ + tl] += bb[e]; ++e; }
+        }
+      }
+      if (NEED_J) {
+        // ---- pass 2: (bottom, top) block -> O
+        double bt[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) bt[i] = 0.0;
+#pragma unroll 1
+        for (int qp = 0; qp < 8; ++qp) {
+          double N[8], G[8][3], g[16], c, d;
+          const double W = hex_point(h, qp, N, G);
+          hex_visc<N3>(h, G, W, kp, g, c, d);
+          hex_accum<1>(G, g, c, d, bt);
+        }
+#pragma unroll
+        for (int i = 0; i < 64; ++i) O[i * TPQ + tl] = bt[i];
+        // ---- pass 3: (top, top) block -> held
+        double tt[36];
+#pragma unroll
+        for (int i = 0; i < 36; ++i) tt[i] = 0.0;
+#pragma unroll 1
+        for (int qp = 0; qp < 8; ++qp) {
+          double N[8], G[8][3], g[16], c, d;
+          const double W = hex_point(h, qp, N, G);
+          hex_visc<N3>(h, G, W, kp, g, c, d);
+          hex_accum<2>(G, g, c, d, tt);
+        }
+        int e = 0;
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp)
+#pragma unroll
+          for (int p2 = pp; p2 < 8; ++p2) { held[dmap4(pp, p2)] = tt[e]; ++e; }
+      }
+    }
+    if (k == 0) bulk_wait(&plan_bar);
+    __syncthreads();
+    if (NEED_J) {
+      if (k < L) phase_bq_j<true>(sp, k, L, D, O, vals, pv.partials, threadIdx.x, blockDim.x);
+    }
+    phase_bq_r(sp, k, L, D + kHexDR * TPQ, R, pv.partials, threadIdx.x, blockDim.x);
+    __syncthreads();
+    if (active) {   // the held top block becomes level k+1's diagonal block
+      if (NEED_J) {
+#pragma unroll
+        for (int i = 0; i < kHexDE; ++i) D[i * TPQ + tl] = held[i];
+      } else {
+#pragma unroll
+        for (int i = kHexDR; i < kHexDE; ++i) D[i * TPQ + tl] = held[i];
+      }
+    }
+  }
+  if (L == 0) bulk_wait(&plan_bar);
+  __syncthreads();
+  if (NEED_J) phase_bq_j<false>(sp, L, L, D, O, vals, pv.partials, threadIdx.x, blockDim.x);
+  phase_bq_r(sp, L, L, D + kHexDR * TPQ, R, pv.partials, threadIdx.x, blockDim.x);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host
@@ -384,6 +685,39 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
   fo_status st = cuda_status(cudaSetDevice(device), "cudaSetDevice");
   if (st) return st;
 
+  // quads in Hilbert order of their centroids (the patch kernel's patches are
+  // runs of consecutive quads, so they come out compact); `order[t]` = the
+  // caller's index of local quad t
+  std::vector<int32_t> order(static_cast<size_t>(n_quad));
+  {
+    double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+    for (int64_t c = 0; c < n_vert; ++c) {
+      x0 = std::min(x0, xy[2 * c]); x1 = std::max(x1, xy[2 * c]);
+      y0 = std::min(y0, xy[2 * c + 1]); y1 = std::max(y1, xy[2 * c + 1]);
+    }
+    const double span = std::max(std::max(x1 - x0, y1 - y0), 1e-300);
+    std::vector<uint64_t> key(static_cast<size_t>(n_quad));
+    for (int64_t t = 0; t < n_quad; ++t) {
+      double cx = 0.0, cy = 0.0;
+      for (int j = 0; j < 4; ++j) { cx += xy[2 * quad[4 * t + j]]; cy += xy[2 * quad[4 * t + j] + 1]; }
+      const uint32_t n = 1u << 16;
+      uint32_t ix = uint32_t(std::min(double(n - 1), (0.25 * cx - x0) / span * double(n)));
+      uint32_t iy = uint32_t(std::min(double(n - 1), (0.25 * cy - y0) / span * double(n)));
+      uint64_t d = 0;   // Hilbert index (xy -> d)
+      for (uint32_t sq = n / 2; sq > 0; sq /= 2) {
+        const uint32_t rx = (ix & sq) > 0, ry = (iy & sq) > 0;
+        d += uint64_t(sq) * sq * ((3 * rx) ^ ry);
+        if (ry == 0) {
+          if (rx == 1) { ix = n - 1 - ix; iy = n - 1 - iy; }
+          std::swap(ix, iy);
+        }
+      }
+      key[size_t(t)] = d;
+      order[size_t(t)] = int32_t(t);
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return key[size_t(a)] < key[size_t(b)]; });
+  }
+
   fo_mesh m = new fo_mesh_s();
   m->device = device;
   m->p = *p;
@@ -399,7 +733,7 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
   m->glob.resize(size_t(n_vert));
   for (int64_t c = 0; c < n_vert; ++c) m->glob[size_t(c)] = c;
   m->tri_glob.resize(size_t(n_quad));
-  for (int64_t t = 0; t < n_quad; ++t) m->tri_glob[size_t(t)] = t;
+  for (int64_t t = 0; t < n_quad; ++t) m->tri_glob[size_t(t)] = order[size_t(t)];
   // coupling lists: every corner of every quad around the column, sorted
   std::vector<std::vector<int32_t>> lists(static_cast<size_t>(n_vert));
   for (int64_t c = 0; c < n_vert; ++c) lists[size_t(c)].push_back(int32_t(c));
@@ -434,10 +768,13 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
     r.beta = floating ? 0.0 : beta[c];
     r.cs_n = (m->colstart[size_t(c)] << 8) | (m->nbr_ptr[size_t(c) + 1] - m->nbr_ptr[size_t(c)]);
   }
-  std::vector<QuadRec> qrec(static_cast<size_t>(n_quad));
+  std::vector<QuadRec>& qrec = m->quadrec;
+  qrec.assign(static_cast<size_t>(n_quad), QuadRec{});
+  m->tri.resize(size_t(4 * n_quad));
   for (int64_t t = 0; t < n_quad; ++t) {
     QuadRec& q = qrec[size_t(t)];
-    for (int i = 0; i < 4; ++i) q.v[i] = quad[4 * t + i];
+    for (int i = 0; i < 4; ++i) q.v[i] = quad[4 * int64_t(order[size_t(t)]) + i];
+    for (int i = 0; i < 4; ++i) m->tri[size_t(4 * t + i)] = q.v[i];
     for (int i = 0; i < 4; ++i) {
       const int32_t* b = m->nbr.data() + m->nbr_ptr[size_t(q.v[i])];
       const int32_t* e = m->nbr.data() + m->nbr_ptr[size_t(q.v[i]) + 1];
@@ -447,13 +784,13 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
   // greedy colouring: quads sharing a corner get different colours
   std::vector<std::vector<int32_t>> vq(static_cast<size_t>(n_vert));
   for (int64_t t = 0; t < n_quad; ++t)
-    for (int i = 0; i < 4; ++i) vq[size_t(quad[4 * t + i])].push_back(int32_t(t));
+    for (int i = 0; i < 4; ++i) vq[size_t(qrec[size_t(t)].v[i])].push_back(int32_t(t));
   std::vector<int32_t> color(size_t(n_quad), -1);
   int ncol = 0;
   for (int64_t t = 0; t < n_quad; ++t) {
     uint64_t taken = 0;
     for (int i = 0; i < 4; ++i)
-      for (int32_t o : vq[size_t(quad[4 * t + i])])
+      for (int32_t o : vq[size_t(qrec[size_t(t)].v[i])])
         if (color[size_t(o)] >= 0 && color[size_t(o)] < 64) taken |= 1ull << color[size_t(o)];
     int c = 0;
     while (c < 64 && ((taken >> c) & 1)) ++c;
@@ -481,15 +818,55 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
   if (!st) st = up(reinterpret_cast<void**>(&m->d_hex_ids), ids.data(), ids.size() * sizeof(int32_t));
   if (!st && A_elem && m->n_elem > 0) {
     std::vector<double> afac(static_cast<size_t>(m->n_elem));
-    for (int64_t i = 0; i < m->n_elem; ++i) {
-      if (!(A_elem[i] > 0.0)) { st = bad(FO_EINVAL, "A_elem must be > 0"); break; }
-      afac[size_t(i)] = std::pow(A_elem[i], -1.0 / p->glen_n);
+    for (int64_t i = 0; i < m->n_elem; ++i) {   // local order: quad t, layer k
+      const double a = A_elem[int64_t(order[size_t(i / L)]) * L + i % L];
+      if (!(a > 0.0)) { st = bad(FO_EINVAL, "A_elem must be > 0"); break; }
+      afac[size_t(i)] = std::pow(a, -1.0 / p->glen_n);
     }
     if (!st) st = up(reinterpret_cast<void**>(&m->d_A), afac.data(), afac.size() * sizeof(double));
     m->has_A_elem = true;
   }
+  if (!st) st = build_patch_plan(m);   // owner-computes patches (KH-patch)
   if (st) { fo_mesh_destroy(m); return st; }
   *out = m;
+  return FO_OK;
+}
+
+// KH-patch: zero fill of boundary columns, the patch kernel, the multi fix-up
+static fo_status launch_hex_owner(fo_mesh m, const double* d_U, double* R, double* d_vals, cudaStream_t s) {
+  int launches = 0;
+  fo_status st = launch_owner_prologue(m, R, d_vals, s, &launches);
+  if (st) return st;
+  const bool n3 = m->p.glen_n == 3.0;
+  const KParams kp = make_kparams(m);
+  PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
+              m->d_plan.blob_off, m->d_plan.partials, 0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
+              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches};
+  const size_t sm = size_t(d_vals ? kPlanOffsetQ : kPlanOffsetQR) + kPlanBytesHex;
+  auto go = [&](auto kern) -> fo_status {
+    fo_status e = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                              "cudaFuncSetAttribute");
+    if (e) return e;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (m->timing) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+    kern<<<m->plan.n_patches, kPatchQuads, sm, s>>>(m->d_col, m->d_quad, m->d_sigma, m->d_A, kp, pv, d_U, R, d_vals);
+    if (m->timing) {
+      cudaEventRecord(e1, s);
+      m->timed.push_back({e0, e1});
+    }
+    return cuda_status(cudaGetLastError(), "kh_patch_kernel launch");
+  };
+  if (d_vals) st = n3 ? go(kh_patch_kernel<true, true>) : go(kh_patch_kernel<true, false>);
+  else st = n3 ? go(kh_patch_kernel<false, true>) : go(kh_patch_kernel<false, false>);
+  if (st) return st;
+  ++launches;
+  st = launch_owner_fixup(m, R, d_vals, s, &launches);
+  if (st) return st;
+  m->last_launches = launches;
   return FO_OK;
 }
 
@@ -503,6 +880,11 @@ fo_status launch_hex(fo_mesh m, const double* d_U, double* d_R, double* d_vals, 
     }
     R = m->d_scratch_R;
   }
+  // R + J: the quad-patch kernel; the residual alone (16 values per
+  // hexahedron) is faster with the coloured read-modify-write, which is also
+  // the R + J ablation (FO_SCATTER_ATOMIC): both deterministic
+  if (need_j && m->scatter != FO_SCATTER_ATOMIC && m->plan.n_patches > 0)
+    return launch_hex_owner(m, d_U, R, d_vals, s);
   fo_status st = cuda_status(cudaMemsetAsync(R, 0, sizeof(double) * m->n_dof, s), "cudaMemsetAsync");
   if (!st && need_j) st = cuda_status(cudaMemsetAsync(d_vals, 0, sizeof(double) * m->nnz, s), "cudaMemsetAsync");
   if (st) return st;

@@ -685,7 +685,8 @@ fo_status fo_set_scatter(fo_mesh m, fo_scatter s) {
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
   if (s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC && s != FO_SCATTER_OWNER_WS && s != FO_SCATTER_OWNER_1WG)
     return fail(FO_EINVAL, "bad scatter");
-  if (m->quad && s != FO_SCATTER_OWNER) return fail(FO_EINVAL, "hexahedra use the coloured scatter");
+  if (m->quad && s != FO_SCATTER_OWNER && s != FO_SCATTER_ATOMIC)
+    return fail(FO_EINVAL, "hexahedra: FO_SCATTER_OWNER (patches) or FO_SCATTER_ATOMIC (coloured ablation)");
   if (s != FO_SCATTER_OWNER && s != FO_SCATTER_OWNER_1WG && m->elem_type != FO_ELEM_WEDGE)
     return fail(FO_EINVAL, "this scatter supports FO_ELEM_WEDGE only");
   m->scatter = s;

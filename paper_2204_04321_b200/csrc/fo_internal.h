@@ -56,6 +56,32 @@ constexpr int kPatchStride = kPatchTris + 1;
 // shared-memory budget of one patch's plan (columns, pairs, contributions)
 constexpr int kPlanBytes = (233472 - 1024 * kPatchCtasPerSm) / kPatchCtasPerSm - 99 * kPatchStride * 8 - 64;
 
+// Hexahedral patches (NEXT-f4 owner-computes, fo_hex.cu): <= kPatchQuads
+// quads per patch, shared memory per quad: D = (bottom,bottom) block of the 8
+// bottom dofs (36, 2x2 node-block layout) + 8 residual entries, O = the 8 x 8
+// (bottom, top) block
+constexpr int kPatchQuads = 96;
+constexpr int kPatchStrideQ = kPatchQuads + 1;
+constexpr int kHexDE = 44, kHexOE = 64;
+constexpr int kHexCtasPerSm = 2;
+constexpr int kPlanBytesHex =
+    (233472 - 1024 * kHexCtasPerSm) / kHexCtasPerSm - (kHexDE + kHexOE) * kPatchStrideQ * 8 - 64;
+
+// Encoded contribution (fo_plan.cpp contrib_code) of an element with NV
+// footprint corners (3: wedge, 4: hexahedron): element slot tl | D base of the
+// (j, j2) 2x2 node block | its stride pattern | O base of (row (j,0), column
+// (j2,0)) | O base of the transpose | j.  Field widths per NV:
+template <int NV>
+struct CodeBits {
+  static constexpr int kTl = NV == 3 ? 8 : 7;    // bits [0, kTl)
+  static constexpr int kDb = 13 - kTl;           // bits [kTl, 13)
+  static constexpr int kPat = 13;                // bits 13-14
+  static constexpr int kOw = NV == 3 ? 5 : 6;
+  static constexpr int kO = 15, kOt = 15 + kOw, kJ = 15 + 2 * kOw;
+  static constexpr int kRow = 2 * NV;            // O row stride (dofs of one level)
+  static constexpr int kDsym = NV * (2 * NV + 1);  // D entries before the residual
+};
+
 // plan records (fo_plan.cpp); copied to shared memory by the kernel
 struct PlanCol {            // 24 bytes
   int64_t colstart;         // CSR value offset of the column's first row
@@ -151,6 +177,7 @@ struct fo_mesh_s {
   std::vector<int32_t> nbr;
   std::vector<int64_t> colstart;   // [n_col+1] CSR value offset of each column block
   std::vector<fo::TriRec> trirec;
+  std::vector<fo::QuadRec> quadrec;   // hexahedral meshes (tri then holds 4 corners per quad)
   std::vector<fo::ColRec> colrec;
   std::vector<double> sigma;
   bool has_A_elem = false;
@@ -232,6 +259,8 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
                           void* stream);
 fo_status build_patch_plan(fo_mesh m, bool upload = true);
 // owner-computes assembly pieces (fo_owner.cu)
+fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
+fo_status launch_owner_fixup(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
 fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
                                cudaStream_t side, cudaEvent_t ev0, cudaEvent_t ev_b);
 void free_patch_plan(fo_mesh m);

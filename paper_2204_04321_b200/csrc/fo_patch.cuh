@@ -1,0 +1,123 @@
+// fo_patch.cuh -- pieces shared by the owner-computes patch kernels of the
+// wedge path (fo_owner.cu) and of the hexahedral path (fo_hex.cu): the view of
+// the patch plan, the one-shot bulk copy of a patch's plan into shared memory,
+// and the emission of one (column, slot) pair's sums into the CSR values
+// ("KA-patch").
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fo_internal.h"
+
+namespace fo {
+
+struct PlanView {
+  const int32_t* __restrict__ t_begin;
+  const int32_t* __restrict__ col_ptr;
+  const int32_t* __restrict__ pair_ptr;
+  const int32_t* __restrict__ nedge;
+  const uint8_t* __restrict__ blob;      // per-patch plan blobs (fo_plan.cpp)
+  const int64_t* __restrict__ blob_off;
+  double* partials;   // multi columns' partial blocks (fo_plan.cpp)
+  int p_off;          // patch of block 0 (a launch covers patches p_off .. p_off + gridDim.x - 1)
+  // KA-ws in-kernel zero fill (inkz != 0, single launch over all patches):
+  // patches are taken in ticket order (flags[n_patches]), each zero-fills the
+  // boundary columns it leads (zl), raises flags[p], and waits for the flags
+  // of the leads of its other boundary columns (wl)
+  const int32_t* __restrict__ zl;
+  const int32_t* __restrict__ zl_ptr;
+  const int32_t* __restrict__ wl;
+  const int32_t* __restrict__ wl_ptr;
+  int32_t* flags;
+  int inkz;
+  int n_patches;
+};
+
+// one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor):
+// bulk_init by one thread, a CTA barrier, then bulk_load by that thread
+__device__ __forceinline__ void bulk_init(uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// The patch's plan in shared memory.
+struct SmemPlan {
+  const PlanCol* cols;
+  const PlanPair* pairs;
+  const uint32_t* contrib;
+  int ncols, npairs;
+  int nedge;   // pairs [0, nedge): edge slots, exactly two entries each
+};
+
+__device__ __forceinline__ void put2(double* dst, double x, double y, bool interior) {
+  if (interior) {
+    *reinterpret_cast<double2*>(dst) = make_double2(x, y);
+  } else {
+    red_add(dst, x);
+    red_add(dst + 1, y);
+  }
+}
+
+// The 12 sums of one (column, slot) pair: level-kk rows x column level kk
+// (dg, from D), level-kk rows x level kk+1 (up, from O), level-kk+1 rows x
+// level kk (nx, from O transposed); [row comp a][column comp b].
+struct PairSums {
+  double dg[4], up[4], nx[4];
+};
+
+// write one pair's sums: plain stores (interior column) or RED (boundary),
+// or the patch's partial block (self slot of a multi column)
+template <bool UP>
+__device__ __forceinline__ void emit(const PlanPair& pp, const PlanCol& pc, const PairSums& s, int kk, int L,
+                                     double* __restrict__ vals, double* __restrict__ partials) {
+  const int m0 = (kk == 0 || kk == L) ? 2 : 3;           // column groups of level-kk rows
+  const int m1 = (kk + 1 == L) ? 2 : 3;                   // column groups of level-kk+1 rows
+  const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
+  const int g0 = kk == 0 ? 0 : 2;                          // offset of group kk in a kk-row slot
+  const int nc = pc.info & 255;
+  const bool interior = (pc.info >> 8) & 1;
+  if (((pc.info >> 30) & 1) && pp.slot == ((pc.info >> 9) & 255)) {
+    double2* q = reinterpret_cast<double2*>(partials + (int64_t(pc.pad) * (L + 1) + kk) * kPartialStride);
+    q[0] = make_double2(s.dg[0], s.dg[1]);
+    q[1] = make_double2(s.dg[2], s.dg[3]);
+    if (UP) {
+      q[2] = make_double2(s.up[0], s.up[1]);
+      q[3] = make_double2(s.up[2], s.up[3]);
+      q[4] = make_double2(s.nx[0], s.nx[1]);
+      q[5] = make_double2(s.nx[2], s.nx[3]);
+    }
+    return;
+  }
+  double* d0 = vals + pc.colstart + int64_t(4 * nc) * P0 + int64_t(pp.slot) * (2 * m0) + g0;
+  double* d1 = d0 + 2 * nc * m0;
+  put2(d0, s.dg[0], s.dg[1], interior);
+  put2(d1, s.dg[2], s.dg[3], interior);
+  if (UP) {
+    put2(d0 + 2, s.up[0], s.up[1], interior);
+    put2(d1 + 2, s.up[2], s.up[3], interior);
+    double* e0 = vals + pc.colstart + int64_t(4 * nc) * P1 + int64_t(pp.slot) * (2 * m1);
+    put2(e0, s.nx[0], s.nx[1], interior);
+    put2(e0 + 2 * nc * m1, s.nx[2], s.nx[3], interior);
+  }
+}
+
+
+}  // namespace fo

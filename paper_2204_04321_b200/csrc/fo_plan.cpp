@@ -56,25 +56,51 @@ struct PatchBuild {
 //   bits 15-19  O index of (row (j,0), column (j2,0)) = 12 j + 2 j2
 //   bits 20-24  O index of (row (j2,0), column (j,0)) = 12 j2 + 2 j (transpose)
 //   bits 25-26  j (residual entry 21 + 2 j + a)
-// The code kPatchTris (tl = kPatchTris, all offsets 0) is the pad entry.
+// The code kPatchTris (tl = kPatchTris, all offsets 0) is the pad entry
+// (kPatchQuads for hexahedra).
+// Hexahedra (NV = 4, CodeBits<4>): the same fields for the 8 bottom dofs of
+// a quad -- off-diagonal node blocks j < j2 at 4 rank(j, j2), diagonal ones
+// at 24 + 3 j, O index 16 j + 2 j2, residual entry 36 + 2 j + a.
+template <int NV>
 uint32_t contrib_code(int tl, int j, int j2) {
+  using CB = CodeBits<NV>;
   uint32_t dbase, pat;
-  if (j == j2) { dbase = 12 + 3 * j; pat = 0; }
-  else { dbase = 4 * (j + j2 - 1); pat = j < j2 ? 1 : 2; }
-  return uint32_t(tl) | (dbase << 8) | (pat << 13) | (uint32_t(12 * j + 2 * j2) << 15) |
-         (uint32_t(12 * j2 + 2 * j) << 20) | (uint32_t(j) << 25);
+  const int lo = j < j2 ? j : j2, hi = j < j2 ? j2 : j;
+  if (j == j2) { dbase = uint32_t(4 * NV * (NV - 1) / 2 + 3 * j); pat = 0; }
+  else { dbase = uint32_t(4 * (lo * (2 * NV - 1 - lo) / 2 + (hi - lo - 1))); pat = j < j2 ? 1 : 2; }
+  return uint32_t(tl) | (dbase << CB::kTl) | (pat << CB::kPat) | (uint32_t(2 * CB::kRow * j + 2 * j2) << CB::kO) |
+         (uint32_t(2 * CB::kRow * j2 + 2 * j) << CB::kOt) | (uint32_t(j) << CB::kJ);
 }
 
-// plan of the triangle range [t0, t1)
+// the corners of element t and the slot of corner j2's column in corner j's list
+template <int NV>
+struct ElemView;
+template <>
+struct ElemView<3> {
+  const fo_mesh m;
+  int32_t corner(int64_t t, int j) const { return m->tri[size_t(3 * t + j)]; }
+  int slot(int64_t t, int j, int j2) const { return m->trirec[size_t(t)].slot[3 * j + j2]; }
+};
+template <>
+struct ElemView<4> {
+  const fo_mesh m;
+  int32_t corner(int64_t t, int j) const { return m->quadrec[size_t(t)].v[j]; }
+  int slot(int64_t t, int j, int j2) const { return m->quadrec[size_t(t)].slot[4 * j + j2]; }
+};
+
+// plan of the element range [t0, t1)
+template <int NV>
 void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int32_t t1,
                PatchBuild& B, std::vector<char>& boundary) {
+  const ElemView<NV> ev{m};
+  const uint32_t kPad = uint32_t(NV == 3 ? kPatchTris : kPatchQuads);   // pad entry: the zero element slot
   B.cols.clear();
   B.pairs.clear();
   B.contrib.clear();
   std::vector<PlanPair> self_pairs;   // appended after the edge pairs (see below)
   std::vector<std::pair<int32_t, int32_t>> inc;   // (column, tl*4 + j)
   for (int32_t t = t0; t < t1; ++t)
-    for (int j = 0; j < 3; ++j) inc.push_back({m->tri[size_t(3 * t + j)], (t - t0) * 4 + j});
+    for (int j = 0; j < NV; ++j) inc.push_back({ev.corner(t, j), (t - t0) * 4 + j});
   std::sort(inc.begin(), inc.end());
   size_t i = 0;
   while (i < inc.size()) {
@@ -89,9 +115,8 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
     std::vector<std::vector<uint32_t>> per_slot(static_cast<size_t>(nc));
     for (size_t q = i; q < e; ++q) {
       const int32_t tl = inc[q].second >> 2, j = inc[q].second & 3;
-      const TriRec& tr = m->trirec[size_t(t0 + tl)];
-      for (int j2 = 0; j2 < 3; ++j2)
-        per_slot[tr.slot[3 * j + j2]].push_back(contrib_code(tl, j, j2));
+      for (int j2 = 0; j2 < NV; ++j2)
+        per_slot[size_t(ev.slot(t0 + tl, j, j2))].push_back(contrib_code<NV>(tl, j, j2));
     }
     PlanCol pc{};
     pc.colstart = m->colstart[size_t(c)];
@@ -102,9 +127,9 @@ void build_one(const fo_mesh m, const std::vector<int32_t>& fan, int32_t t0, int
       auto& l = per_slot[size_t(s)];
       // even lengths: phase B gathers two contributions per step; the pad
       // entry reads triangle slot kPatchTris, kept zero by the kernel
-      if (l.size() & 1) l.push_back(uint32_t(kPatchTris));
+      if (l.size() & 1) l.push_back(kPad);
       if (s != self && (interior || !l.empty()))   // edge slots: exactly two entries
-        while (l.size() < 2) l.push_back(uint32_t(kPatchTris));   // (interior slots of a part mesh may have none)
+        while (l.size() < 2) l.push_back(kPad);   // (interior slots of a part mesh may have none)
       if (l.empty() && !interior) continue;   // boundary: only touched slots
       PlanPair pp{};
       pp.cnt = uint8_t(l.size());
@@ -157,9 +182,10 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
   const int64_t nt = m->n_tri;
   const int64_t nk = m->nA + m->nB;     // columns with rows
   if (nt == 0) return FO_OK;
+  const int nv = m->quad ? 4 : 3;
   std::vector<int32_t> fan(size_t(m->n_col), 0);
   for (int64_t t = 0; t < nt; ++t)
-    for (int j = 0; j < 3; ++j) fan[size_t(m->tri[size_t(3 * t + j)])]++;
+    for (int j = 0; j < nv; ++j) fan[size_t(m->tri[size_t(nv * t + j)])]++;
   std::vector<char> boundary(size_t(nk), 0);
   P.t_begin.assign(1, 0);
   P.col_ptr.assign(1, 0);
@@ -167,9 +193,11 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
   P.contrib_ptr.assign(1, 0);
   PatchBuild B;
   int64_t t0 = 0;
-  // equal-size ranges of at most kPatchTris triangles; a range whose plan
-  // exceeds the shared-memory budget is halved
-  const int64_t np0 = (nt + kPatchTris - 1) / kPatchTris;
+  // equal-size ranges of at most kPatchTris triangles (kPatchQuads quads); a
+  // range whose plan exceeds the shared-memory budget is halved
+  const int64_t per_patch = m->quad ? kPatchQuads : kPatchTris;
+  const size_t budget = size_t(m->quad ? kPlanBytesHex : kPlanBytes);
+  const int64_t np0 = (nt + per_patch - 1) / per_patch;
   std::vector<int64_t> bounds;
   for (int64_t p = 0; p <= np0; ++p) bounds.push_back((p * nt) / np0);
   for (size_t b = 0; b + 1 < bounds.size(); ++b) {
@@ -178,8 +206,9 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
       auto [a0, a1] = todo.back();
       todo.pop_back();
       std::vector<char> bnd_tmp = boundary;
-      build_one(m, fan, int32_t(a0), int32_t(a1), B, bnd_tmp);
-      if (plan_bytes(B) > size_t(kPlanBytes) && a1 - a0 > 1) {
+      if (m->quad) build_one<4>(m, fan, int32_t(a0), int32_t(a1), B, bnd_tmp);
+      else build_one<3>(m, fan, int32_t(a0), int32_t(a1), B, bnd_tmp);
+      if (plan_bytes(B) > budget && a1 - a0 > 1) {
         const int64_t mid = (a0 + a1) / 2;
         todo.push_back({mid, a1});
         todo.push_back({a0, mid});
@@ -329,7 +358,9 @@ fo_status plan_check(const fo_mesh m, int64_t* stats) {
   std::vector<char> zeroed(size_t(m->n_col), 0), multi(size_t(m->n_col), 0);
   for (int32_t c : P.zero_cols) zeroed[size_t(c)] = 1;
   for (const MultiRec& r : P.multi) multi[size_t(r.c)] = 1;
-  std::vector<int32_t> seen(size_t(9 * m->n_tri), 0);
+  const bool quad = m->quad;
+  const int nv = quad ? 4 : 3;
+  std::vector<int32_t> seen(size_t(nv * nv * m->n_tri), 0);
   int64_t n_contrib = 0, bad_elem = 0;
   for (int32_t p = 0; p < P.n_patches; ++p) {
     const PlanCol* cols = P.cols.data() + P.col_ptr[size_t(p)];
@@ -350,16 +381,21 @@ fo_status plan_check(const fo_mesh m, int64_t* stats) {
       for (int i = 0; i < pp.cnt; ++i) {
         const uint32_t cb = i == 0 ? pp.c0 : i == 1 ? pp.c1
                                     : P.contrib[size_t(P.contrib_ptr[size_t(p)] + pp.off + i - 2)];
-        const int tl = int(cb & 255);
-        if (tl == kPatchTris) continue;   // pad
+        // decode with the element's field layout (CodeBits<3> / <4>)
+        const int tlb = quad ? CodeBits<4>::kTl : CodeBits<3>::kTl;
+        const int ob = CodeBits<3>::kO, ow = quad ? CodeBits<4>::kOw : CodeBits<3>::kOw;
+        const int jb = quad ? CodeBits<4>::kJ : CodeBits<3>::kJ, row = 2 * nv;
+        const int tl = int(cb & ((1u << tlb) - 1));
+        if (tl == (quad ? kPatchQuads : kPatchTris)) continue;   // pad
         ++n_contrib;
-        const int j = int((cb >> 25) & 3);
-        const int o = int((cb >> 15) & 31);   // 12 j + 2 j2
-        const int j2 = (o - 12 * j) / 2;
+        const int j = int((cb >> jb) & 3);
+        const int o = int((cb >> ob) & ((1u << ow) - 1));   // 2 row j + 2 j2
+        const int j2 = (o - 2 * row * j) / 2;
         const int64_t t = t0 + tl;
-        const TriRec& tr = m->trirec[size_t(t)];
-        if (tr.v[j] != pc.c || tr.slot[3 * j + j2] != pp.slot) ++bad_elem;
-        seen[size_t(9 * t + 3 * j + j2)]++;
+        const int32_t vj = quad ? m->quadrec[size_t(t)].v[j] : m->trirec[size_t(t)].v[j];
+        const int sl = quad ? m->quadrec[size_t(t)].slot[4 * j + j2] : m->trirec[size_t(t)].slot[3 * j + j2];
+        if (vj != pc.c || sl != pp.slot) ++bad_elem;
+        seen[size_t(nv * nv * t + nv * j + j2)]++;
       }
     }
     for (int32_t ci = P.col_ptr[size_t(p)]; ci < P.col_ptr[size_t(p) + 1]; ++ci) {
