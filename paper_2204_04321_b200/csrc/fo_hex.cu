@@ -41,42 +41,51 @@ struct HexIn {
   double Afac;
 };
 
-// basis, physical gradients G and weight W = det J at Gauss point qp
+// basis, physical gradients G and weight W = det J at Gauss point qp, using
+// the column structure of the extruded hexahedron: x, y depend on (xi, eta)
+// only, so J = [[A, 0], [c^T, z_zeta]] with A the 2 x 2 footprint Jacobian and
+// c = (z_xi, z_eta); det J = det A z_zeta and, with N_(j,l) = Q_j(xi, eta)
+// f_l(zeta), f_l' = s_l = -1/2, +1/2:
+//   grad_xy N_(j,l) = f_l P_j + s_l Q_j K,  P_j = A^-T grad_(xi,eta) Q_j,
+//   K = -A^-T c / z_zeta,   d/dz N_(j,l) = s_l Q_j / z_zeta
+// (exactly the isoparametric gradient; no general 3 x 3 inverse)
 __device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8], double G[8][3]) {
   constexpr double gz = 0.57735026918962576451;
   const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
   const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
-  double dN[8][3];
-  double J00 = 0, J01 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0, J20 = 0, J21 = 0, J22 = 0;
+  const double f0 = 0.5 * (1.0 - zeta), f1 = 0.5 * (1.0 + zeta);
+  double Q[4], Qx[4], Qe[4];
+  double xx = 0, xe = 0, yx = 0, ye = 0, zx = 0, ze = 0, zz = 0;
 #pragma unroll
-  for (int l = 0; l < 2; ++l)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = j + 4 * l;
-      const double fq = 0.25 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
-      const double fz = l == 0 ? 0.5 * (1.0 - zeta) : 0.5 * (1.0 + zeta);
-      N[i] = fq * fz;
-      dN[i][0] = 0.25 * cxi[j] * (1.0 + ceta[j] * eta) * fz;
-      dN[i][1] = 0.25 * ceta[j] * (1.0 + cxi[j] * xi) * fz;
-      dN[i][2] = fq * (l == 0 ? -0.5 : 0.5);
-      const double z = l == 0 ? h.Zb[j] : h.Zt[j];
-      J00 = fma(h.X[j], dN[i][0], J00); J01 = fma(h.X[j], dN[i][1], J01); J02 = fma(h.X[j], dN[i][2], J02);
-      J10 = fma(h.Y[j], dN[i][0], J10); J11 = fma(h.Y[j], dN[i][1], J11); J12 = fma(h.Y[j], dN[i][2], J12);
-      J20 = fma(z, dN[i][0], J20); J21 = fma(z, dN[i][1], J21); J22 = fma(z, dN[i][2], J22);
-    }
-  const double c00 = J11 * J22 - J12 * J21, c01 = J12 * J20 - J10 * J22, c02 = J10 * J21 - J11 * J20;
-  const double det = J00 * c00 + J01 * c01 + J02 * c02;
-  const double id = 1.0 / det;
-  const double i00 = c00 * id, i01 = (J02 * J21 - J01 * J22) * id, i02 = (J01 * J12 - J02 * J11) * id;
-  const double i10 = c01 * id, i11 = (J00 * J22 - J02 * J20) * id, i12 = (J02 * J10 - J00 * J12) * id;
-  const double i20 = c02 * id, i21 = (J01 * J20 - J00 * J21) * id, i22 = (J00 * J11 - J01 * J10) * id;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    G[i][0] = i00 * dN[i][0] + i10 * dN[i][1] + i20 * dN[i][2];
-    G[i][1] = i01 * dN[i][0] + i11 * dN[i][1] + i21 * dN[i][2];
-    G[i][2] = i02 * dN[i][0] + i12 * dN[i][1] + i22 * dN[i][2];
+  for (int j = 0; j < 4; ++j) {
+    const double ax = 1.0 + cxi[j] * xi, ae = 1.0 + ceta[j] * eta;
+    Q[j] = 0.25 * ax * ae;
+    Qx[j] = 0.25 * cxi[j] * ae;
+    Qe[j] = 0.25 * ceta[j] * ax;
+    const double zm = fma(f0, h.Zb[j], f1 * h.Zt[j]);
+    xx = fma(h.X[j], Qx[j], xx); xe = fma(h.X[j], Qe[j], xe);
+    yx = fma(h.Y[j], Qx[j], yx); ye = fma(h.Y[j], Qe[j], ye);
+    zx = fma(zm, Qx[j], zx); ze = fma(zm, Qe[j], ze);
+    zz = fma(Q[j], 0.5 * (h.Zt[j] - h.Zb[j]), zz);
   }
-  return det;   // Gauss weights 1
+  const double detA = xx * ye - xe * yx;
+  const double ia = 1.0 / detA, iz = 1.0 / zz;
+  // A^-T = ia [[ye, -yx], [-xe, xx]]
+  const double kx = -(ye * zx - yx * ze) * ia * iz, ky = -(xx * ze - xe * zx) * ia * iz;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double px = (ye * Qx[j] - yx * Qe[j]) * ia, py = (xx * Qe[j] - xe * Qx[j]) * ia;
+    const double hq = 0.5 * Q[j];
+    N[j] = Q[j] * f0;
+    N[j + 4] = Q[j] * f1;
+    G[j][0] = fma(f0, px, -hq * kx);
+    G[j][1] = fma(f0, py, -hq * ky);
+    G[j][2] = -hq * iz;
+    G[j + 4][0] = fma(f1, px, hq * kx);
+    G[j + 4][1] = fma(f1, py, hq * ky);
+    G[j + 4][2] = hq * iz;
+  }
+  return detA * zz;   // Gauss weights 1
 }
 
 // viscosity factors and the strain-rate gradients g_{a,i} = eps_a . grad phi_i
@@ -366,22 +375,17 @@ __device__ __forceinline__ void hex_accum(const double G[8][3], const double g[1
     for (int i2 = c0; i2 < c0 + 4; ++i2) {
       if (BLK != 1 && i2 < i) continue;
       const double gx = G[i2][0], gy = G[i2][1], gz = G[i2][2];
-      const double uu = fma(du, g[2 * i2], fma(az, gz, fma(ay, gy, ax * gx)));
-      const double uv = fma(du, g[2 * i2 + 1], fma(ay, gx, cx * gy));
-      const double vv = fma(dv, g[2 * i2 + 1], fma(az, gz, fma(by, gy, bx * gx)));
       const int p = 2 * (i - r0), p2 = 2 * (i2 - c0);
-      if (BLK == 1) {
-        const double vu = fma(dv, g[2 * i2], fma(cy, gx, bx * gy));
-        acc[8 * p + p2] += uu;
-        acc[8 * p + p2 + 1] += uv;
-        acc[8 * (p + 1) + p2] += vu;
-        acc[8 * (p + 1) + p2 + 1] += vv;
-      } else {
-        auto sym = [](int a, int b) { return a * 8 - (a * (a - 1)) / 2 + (b - a); };
-        acc[sym(p, p2)] += uu;
-        acc[sym(p, p2 + 1)] += uv;
-        acc[sym(p + 1, p2 + 1)] += vv;
-        if (i2 != i) acc[sym(p + 1, p2)] += fma(dv, g[2 * i2], fma(cy, gx, bx * gy));
+      auto sym = [](int a, int b) { return a * 8 - (a * (a - 1)) / 2 + (b - a); };
+      double& euu = BLK == 1 ? acc[8 * p + p2] : acc[sym(p, p2)];
+      double& euv = BLK == 1 ? acc[8 * p + p2 + 1] : acc[sym(p, p2 + 1)];
+      double& evv = BLK == 1 ? acc[8 * (p + 1) + p2 + 1] : acc[sym(p + 1, p2 + 1)];
+      euu = fma(du, g[2 * i2], fma(az, gz, fma(ay, gy, fma(ax, gx, euu))));
+      euv = fma(du, g[2 * i2 + 1], fma(ay, gx, fma(cx, gy, euv)));
+      evv = fma(dv, g[2 * i2 + 1], fma(az, gz, fma(by, gy, fma(bx, gx, evv))));
+      if (BLK == 1 || i2 != i) {
+        double& evu = BLK == 1 ? acc[8 * (p + 1) + p2] : acc[sym(p + 1, p2)];
+        evu = fma(dv, g[2 * i2], fma(cy, gx, fma(bx, gy, evu)));
       }
     }
   }

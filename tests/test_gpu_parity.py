@@ -164,17 +164,25 @@ def test_parity_tetrahedra(torch_cuda, ora_mod, case):
     check_parity(ora_mod.Oracle(fp), g, fp=fp)
 
 
-@pytest.mark.parametrize("case", ["C1-quads", "slab-quads-distorted", "quads-temperature"])
-def test_parity_hexahedra(torch_cuda, ora_mod, case):
+@pytest.mark.parametrize("scatter", [0, 1])
+@pytest.mark.parametrize("case", ["C1-quads", "slab-quads-distorted", "quads-temperature", "quads-40x40",
+                                  "quads-33x33-distorted"])
+def test_parity_hexahedra(torch_cuda, ora_mod, case, scatter):
     """NEXT-f4: quadrilateral footprint, 8-node trilinear hexahedra (P:478,
-    reading L23), coloured deterministic scatter."""
+    reading L23): the quad-patch owner-computes kernel (scatter 0; the 40 x 40
+    and 33 x 33 footprints span 17 / 12 patches, so boundary, multi and pad
+    handling are exercised) and the coloured read-modify-write ablation (1)."""
     if case == "C1-quads":
         fp = mg.to_quads(mg.ismip_hom_a(nx=10, n_layers=5), 10)
     elif case == "slab-quads-distorted":
         fp = mg.to_quads(mg.slab(nx=7, n_layers=4, distort=0.2), 7)
+    elif case == "quads-40x40":
+        fp = mg.to_quads(mg.ismip_hom_a(nx=40, n_layers=3), 40)
+    elif case == "quads-33x33-distorted":
+        fp = mg.to_quads(mg.slab(nx=33, n_layers=2, distort=0.2), 33)
     else:
         fp = mg.with_temperature(mg.to_quads(mg.ismip_hom_a(nx=6, n_layers=3), 6))
-    g = gpu_assemble(torch_cuda, fp)
+    g = gpu_assemble(torch_cuda, fp, scatter=scatter)
     check_parity(ora_mod.Oracle(fp), g, fp=fp)
     import torch
     R2, V2 = g["mesh"].jacobian(torch.tensor(fp.U, device="cuda"))
