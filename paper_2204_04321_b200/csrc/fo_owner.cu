@@ -344,7 +344,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <bool N3>
+template <bool N3, bool TET>
 __global__ void __launch_bounds__(kWsThreads, 2)
 ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
              const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp, PlanView pv,
@@ -417,7 +417,8 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
         const double Afac = wedge_afac(kp, Aw, t0 + te, k);
         WedgeIn w;
         wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
-        wedge_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
+        if constexpr (TET) tet3_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
+        else wedge_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
       }
       double dk[27];
       tmem::wait_st();
@@ -559,11 +560,11 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
 
 static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
-template <bool N3>
+template <bool N3, bool TET>
 static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np,
                            bool inkz) {
   const size_t sm = size_t(kPlanOffsetWS) + kPlanBytes;
-  fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3, TET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sm)), "cudaFuncSetAttribute");
   if (st) return st;
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
@@ -575,7 +576,7 @@ static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, 
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  ka_ws_kernel<N3><<<np, kWsThreads, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R,
+  ka_ws_kernel<N3, TET><<<np, kWsThreads, sm, s>>>(m->d_col, m->d_tri, m->d_sigma, m->d_A, make_kparams(m), pv, U, R,
                                               vals);
   if (m->timing) {
     cudaEventRecord(e1, s);
@@ -645,8 +646,7 @@ fo_status owner_begin(OwnerCall& c, fo_mesh m, const double* d_U, double* d_R, d
 
 // the wedge R + J path runs the warp-specialised kernel unless the round-1 kernel is asked for
 bool uses_ws(const OwnerCall& c) {
-  return c.vals != nullptr && c.m->elem_type != FO_ELEM_TET3 &&
-         (c.m->scatter == FO_SCATTER_OWNER || c.m->scatter == FO_SCATTER_OWNER_WS);
+  return c.vals != nullptr && (c.m->scatter == FO_SCATTER_OWNER || c.m->scatter == FO_SCATTER_OWNER_WS);
 }
 
 // inkz: the warp-specialised kernel zero-fills the boundary columns itself
@@ -683,8 +683,10 @@ fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1, bool inkz 
   const int np = p1 - p0;
   fo_status st;
   if (uses_ws(c))
-    st = n3 ? launch_ws<true>(m, c.U, c.R, c.vals, s, p0, np, inkz)
-            : launch_ws<false>(m, c.U, c.R, c.vals, s, p0, np, inkz);
+    st = tet ? (n3 ? launch_ws<true, true>(m, c.U, c.R, c.vals, s, p0, np, inkz)
+                   : launch_ws<false, true>(m, c.U, c.R, c.vals, s, p0, np, inkz))
+             : (n3 ? launch_ws<true, false>(m, c.U, c.R, c.vals, s, p0, np, inkz)
+                   : launch_ws<false, false>(m, c.U, c.R, c.vals, s, p0, np, inkz));
   else if (need_j)
     st = tet ? (n3 ? launch_patch<true, true, true>(m, c.U, c.R, c.vals, s, p0, np)
                    : launch_patch<true, false, true>(m, c.U, c.R, c.vals, s, p0, np))
