@@ -115,6 +115,26 @@ __device__ __forceinline__ void wedge_input(const TriGeo& g, const TriRec& tr,
   w.go = go;
 }
 
+// wedge_input with the velocities already in registers (bottom / top level)
+__device__ __forceinline__ void wedge_input_u(const TriGeo& g, const double* __restrict__ sigma, double Afac,
+                                              const double2 (&ub)[3], const double2 (&ut)[3], int k, WedgeIn& w,
+                                              bool go = true) {
+  const double sk = __ldg(sigma + k), sk1 = __ldg(sigma + k + 1);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    w.a[j] = g.a[j]; w.b[j] = g.b[j];
+    w.zb[j] = fma(sk, g.H[j], g.base[j]);
+    w.zt[j] = fma(sk1, g.H[j], g.base[j]);
+    w.beta[j] = g.beta[j];
+    w.ub[j] = ub[j].x; w.vb[j] = ub[j].y; w.ut[j] = ut[j].x; w.vt[j] = ut[j].y;
+  }
+  w.D = g.D; w.e1x = g.e1x; w.e1y = g.e1y; w.e2x = g.e2x; w.e2y = g.e2y;
+  w.sx = g.sx; w.sy = g.sy;
+  w.Afac = Afac;
+  w.basal = (k == 0);
+  w.go = go;
+}
+
 // convenience for the one-thread-per-wedge kernels
 __device__ __forceinline__ void load_wedge(const ColRec* __restrict__ col,
                                            const TriRec* __restrict__ tris,

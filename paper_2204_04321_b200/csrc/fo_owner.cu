@@ -335,6 +335,8 @@ constexpr int kWsThreads = 256;
 // (208 / 48 spilled the scatter's addresses: C3 1.471 vs 1.403 ms; 192 / 64: 1.496)
 constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;
 constexpr int kPlanOffsetWS = ((kD + kO) * TP * 8 + 15) / 16 * 16;
+constexpr int kUbufOffsetWS = (kPlanOffsetWS + kPlanBytes + 15) / 16 * 16;   // [3 levels x 3 nodes][TP] double2
+constexpr int kWsSmem = kUbufOffsetWS + 9 * TP * 16;
 constexpr int kBarEmpty = 1, kBarFull = 2, kBarElem = 3, kBarScat = 4;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -407,16 +409,42 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       for (int i = 0; i < 27; ++i) z[i] = 0.0;
       tmem::st<27>(tm + kTmHeld, z);   // no wedge below the bed
     }
+    // the velocities one layer ahead: level k + 2 is copied global -> shared
+    // with cp.async (no registers held) while wedge k is computed, into a
+    // three-level ring per thread (the gather otherwise waits on L2 every layer)
+    double2* const ub2 = reinterpret_cast<double2*>(smem + kUbufOffsetWS / 8);
+    auto u_copy = [&](int lev) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ub2 + ((lev % 3) * 3 + j) * TP + tl));
+        const double2* src = reinterpret_cast<const double2*>(U) + int64_t(tr.v[j]) * (L + 1) + lev;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+      }
+    };
+    u_copy(0);
+    u_copy(1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     for (int k = 0; k < L; ++k) {
       double acc[36];
       {
+        if (k + 2 <= L) u_copy(k + 2);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");   // levels k, k + 1 are in
         const ColRec* colk = col;
         asm volatile("" : "+l"(colk));
         TriGeo geo;
         load_tri_geo(colk, tr, geo);
         const double Afac = wedge_afac(kp, Aw, t0 + te, k);
         WedgeIn w;
-        wedge_input(geo, tr, sigma, Afac, U, L, k, w, kp.go != 0);
+        {
+          double2 ucur[3], utop[3];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            ucur[j] = ub2[((k % 3) * 3 + j) * TP + tl];
+            utop[j] = ub2[(((k + 1) % 3) * 3 + j) * TP + tl];
+          }
+          wedge_input_u(geo, sigma, Afac, ucur, utop, k, w, kp.go != 0);
+        }
         if constexpr (TET) tet3_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
         else wedge_element_ws<N3>(w, kp.rg, kp.eps, kp.glen_n, tm, acc);
       }
@@ -563,7 +591,7 @@ static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPl
 template <bool N3, bool TET>
 static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np,
                            bool inkz) {
-  const size_t sm = size_t(kPlanOffsetWS) + kPlanBytes;
+  const size_t sm = size_t(kWsSmem);
   fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3, TET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sm)), "cudaFuncSetAttribute");
   if (st) return st;
