@@ -327,7 +327,13 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
 // Handshake per level with two named barriers of 256 threads: EMPTY (WG1
 // arrives after its phase B; WG0 waits before overwriting D / O) and FULL (WG0
 // arrives after publishing D(k) / O(k); WG1 waits before its phase B).
-constexpr int kWsThreads = 256;
+// element threads per CTA (one per triangle of a patch, rounded up to
+// warpgroups) and as many scatter threads; 128-triangle patches: 2 CTAs per
+// SM; 255-triangle patches (FO_EXPERIMENT_PATCH255): one 512-thread CTA
+constexpr int kWsHalf = kPatchTris <= 128 ? 128 : 256;
+constexpr int kWsThreads = 2 * kWsHalf;
+constexpr int kWsCtas = kWsHalf == 128 ? 2 : 1;
+constexpr uint32_t kWsAlloc = kTmCols * (kWsHalf / 128);   // TMEM columns per CTA
 #ifndef FO_WS_REGS_E
 #define FO_WS_REGS_E 200
 #endif
@@ -347,7 +353,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 }
 
 template <bool N3, bool TET>
-__global__ void __launch_bounds__(kWsThreads, 2)
+__global__ void __launch_bounds__(kWsThreads, kWsCtas)
 ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
              const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp, PlanView pv,
              const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
@@ -377,9 +383,9 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     sp.nedge = __ldg(pv.nedge + p);
   }
   if (threadIdx.x == 0) bulk_init(&plan_bar);
-  if (threadIdx.x < 32) tmem::alloc(&tmem_base, kTmCols);   // warp 0 owns the TMEM allocation
+  if (threadIdx.x < 32) tmem::alloc(&tmem_base, kWsAlloc);   // warp 0 owns the TMEM allocation
   {   // triangle slot kPatchTris: the zero column the plan's pad entries read
-    const int i = int(threadIdx.x) - 128;
+    const int i = int(threadIdx.x) - kWsHalf;
     if (i >= 0 && i < kD) D[i * TP + kPatchTris] = 0.0;
     if (i >= 0 && i < kO) O[i * TP + kPatchTris] = 0.0;
   }
@@ -388,7 +394,7 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   tmem::fence_after();
   if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   const int L = kp.L;
-  if (threadIdx.x < 128) {
+  if (threadIdx.x < kWsHalf) {
     // ---------------- WG0: elements ----------------
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsE));
     const int tl = threadIdx.x;
@@ -396,7 +402,8 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
     // tcgen05.ld / st are warp-collective: lanes without a triangle evaluate a
     // copy of the patch's last one and publish nothing
     const int te = active ? tl : nt - 1;
-    const uint32_t tm = tmem_base + (uint32_t(tl & ~31) << 16);   // this warp's TMEM lane quarter
+    // this warp's TMEM lane quarter (and, for a second element warpgroup, its column half)
+    const uint32_t tm = tmem_base + (uint32_t(tl & 127 & ~31) << 16) + uint32_t(tl >> 7) * kTmCols;
     TriRec tr;
     {
       const int* tp = reinterpret_cast<const int*>(tris + (t0 + te));
@@ -474,20 +481,20 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       named_arrive(kBarFull, kWsThreads);
     }
     tmem::fence_before();
-    named_sync(kBarElem, 128);   // every element warp is done with TMEM
+    named_sync(kBarElem, kWsHalf);   // every element warp is done with TMEM
     tmem::fence_after();
-    if (tl < 32) tmem::dealloc(tmem_base, kTmCols);
+    if (tl < 32) tmem::dealloc(tmem_base, kWsAlloc);
   } else {
     // ---------------- WG1: scatter (phase B) ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsB));
-    const int tb = int(threadIdx.x) - 128;
+    const int tb = int(threadIdx.x) - kWsHalf;
     if (pv.inkz) {
       // while the element warps compute layer 0: zero-fill the boundary
       // columns this patch leads (a warp per column), publish, then wait for
       // the leads of the other boundary columns before the first RED
       const int z0 = __ldg(pv.zl_ptr + p), z1 = __ldg(pv.zl_ptr + p + 1);
       const int lane = tb & 31;
-      for (int i = z0 + (tb >> 5); i < z1; i += 4) {
+      for (int i = z0 + (tb >> 5); i < z1; i += kWsHalf / 32) {
         const int c = __ldg(pv.zl + i);
         for (int j = lane; j < L + 1; j += 32)
           *reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)) = make_double2(0.0, 0.0);
@@ -496,13 +503,13 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
         const int64_t len2 = int64_t(2 * (csn & 255)) * (3 * L + 1);
         for (int64_t j = lane; j < len2; j += 32) v[j] = make_double2(0.0, 0.0);
       }
-      named_sync(kBarScat, 128);
+      named_sync(kBarScat, kWsHalf);
       if (tb == 0) {
         __threadfence();   // the scatter warps' zero stores (ordered by the barrier) before the flag
         asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(pv.flags + p), "r"(1) : "memory");
       }
       const int w0 = __ldg(pv.wl_ptr + p), w1 = __ldg(pv.wl_ptr + p + 1);
-      for (int i = w0 + tb; i < w1; i += 128) {
+      for (int i = w0 + tb; i < w1; i += kWsHalf) {
         const int32_t* f = pv.flags + __ldg(pv.wl + i);
         int v = 0;
         for (;;) {
@@ -511,17 +518,18 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
           __nanosleep(64);
         }
       }
-      named_sync(kBarScat, 128);
+      named_sync(kBarScat, kWsHalf);
     }
     bulk_wait(&plan_bar);
     named_arrive(kBarEmpty, kWsThreads);   // D / O start free
     for (int kk = 0; kk <= L; ++kk) {
       named_sync(kBarFull, kWsThreads);
-      phase_b<true>(sp, kk, L, D, O, R, vals, pv.partials, tb, 128);
+      phase_b<true>(sp, kk, L, D, O, R, vals, pv.partials, tb, kWsHalf);
       if (kk < L) named_arrive(kBarEmpty, kWsThreads);
     }
   }
 }
+
 
 // zero the rows (CSR values and residual) of boundary columns
 __global__ void zero_boundary_kernel(const ColRec* __restrict__ col, const int32_t* __restrict__ zc,
