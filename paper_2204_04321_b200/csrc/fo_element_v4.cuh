@@ -31,14 +31,6 @@
 
 #include "fo_element.cuh"
 
-#ifndef FO_UNROLL_R1A
-#define FO_UNROLL_R1A 2   // trips of the (bottom, top) rank-1 loop unrolled
-#endif
-#ifndef FO_UNROLL_R1B
-#define FO_UNROLL_R1B 2   // trips of the merged (bottom,bottom)+(top,top) loop unrolled
-#endif
-#define FO_PRAGMA(x) _Pragma(#x)
-#define FO_UNROLL(n) FO_PRAGMA(unroll n)
 
 namespace fo {
 
@@ -180,14 +172,9 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
         // strain-rate vectors
         const double e1x = 2.0 * ux + vy, e1y = exy, e1z = exz;
         const double e2x = exy, e2y = ux + 2.0 * vy, e2z = eyz;
-#ifndef FO_Q_UNSCALED   // default: stored as rho_a Q / 6: r_j Q = (j == a ? 4 : 1) x the stored value
         const double r6 = rho[a] * kSixth;
         Qu(q) = (e1z - e1x * zx - e1y * zy) * r6;
         Qv(q) = (e2z - e2x * zx - e2y * zy) * r6;
-#else
-        Qu(q) = e1z - e1x * zx - e1y * zy;
-        Qv(q) = e2z - e2x * zx - e2y * zy;
-#endif
         E1x(q) = e1x; E1y(q) = e1y; E2y(q) = e2y;   // e2x == e1y
       }
     }
@@ -307,7 +294,6 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
       return fma(Fv, AA, fma(-sg, G1, fma(-sg2, G2, sg * sg2 * KKuv[kk])));
     }
   };
-#ifndef FO_HPART_SINGLE
   // the four level blocks of one (row comp ca, node j; column comp cb, node
   // j2) entry from shared pieces: entry(l, l2) = F_{l+l2} AA - s(l2) Rt(l)
   // - s(l) Ct(l2) + s(l) s(l2) KK with s(0) = -1, s(1) = +1 (the terms of hpart)
@@ -354,7 +340,6 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     e00 = fma(F[0], AA, KK + (Rt[0] + Ct[0]));
     e11 = fma(F[2], AA, KK - (Rt[1] + Ct[1]));
   };
-#endif
   // The sections below are wrapped in `if (w.go)` (always true at run time):
   // branch boundaries keep ptxas from interleaving them, and each rank-1
   // block reads d_q as fma(0, gate, d_q) with gate = a result of the previous
@@ -375,7 +360,6 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
 #pragma unroll
           for (int cb = 0; cb < 2; ++cb) {
             const int p = 2 * j + ca, p2 = 2 * j2 + cb;
-#ifndef FO_HPART_SINGLE   // default: the four level blocks of an entry together
             double e00, e01, e10, e11;
             hpart4(ca, j, cb, j2, e00, e01, e10, e11);
             if (p <= p2) {
@@ -385,16 +369,6 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
             sink.off(p, p2, e01);
             gate = e01;
             if (j != j2) sink.off(p2, p, e10);
-#else
-            if (p <= p2) {
-              sink.top(pk6(p, p2), hpart(ca, j, 1, cb, j2, 1));
-              sink.bot_add(p, p2, hpart(ca, j, 0, cb, j2, 0));
-            }
-            const double v = hpart(ca, j, 0, cb, j2, 1);
-            sink.off(p, p2, v);
-            gate = v;
-            if (j != j2) sink.off(p2, p, hpart(cb, j2, 0, ca, j, 1));
-#endif
           }
       }
   }
@@ -404,7 +378,7 @@ __device__ __forceinline__ void wedge_element_v4(const WedgeIn& w, double rg, do
     for (int p = 0; p < 6; ++p)
 #pragma unroll
       for (int p2 = 0; p2 < 6; ++p2) acc[6 * p + p2] = sink.off_get(p, p2);
-FO_UNROLL(FO_UNROLL_R1A)
+#pragma unroll 2
     for (int q = 0; q < 6; ++q) {   // rolled: not all six points' data live at once
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
@@ -412,18 +386,11 @@ FO_UNROLL(FO_UNROLL_R1A)
       const double f0 = 0.5 - 0.5 * zeta, f1 = 0.5 + 0.5 * zeta;
       const double dg = fma(0.0, gate, dq(q));
       double gb[6], gt[6];
-#ifndef FO_Q_UNSCALED
       const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
       (void)rho_a;
-#endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-#ifndef FO_Q_UNSCALED
         const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
-#else
-        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
-        const double qu = rj * Qu(q), qv = rj * Qv(q);
-#endif
         const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
         const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
         gb[2 * j] = dg * fma(f0, pu, -qu);
@@ -453,7 +420,7 @@ FO_UNROLL(FO_UNROLL_R1A)
     for (int i = 0; i < 21; ++i) at[i] = sink.top_get(i);
 #pragma unroll
     for (int i = 0; i < 6; ++i) rb[i] = rt[i] = 0.0;
-FO_UNROLL(FO_UNROLL_R1B)
+#pragma unroll 2
     for (int q = 0; q < 6; ++q) {
       const int a = q >> 1;
       const double rho_a = a == 0 ? rho[0] : (a == 1 ? rho[1] : rho[2]);
@@ -462,18 +429,11 @@ FO_UNROLL(FO_UNROLL_R1B)
       const double dd = fma(0.0, gate, dq(q));
       const double cc = q == 0 ? cq[0] : q == 1 ? cq[1] : q == 2 ? cq[2] : q == 3 ? cq[3] : q == 4 ? cq[4] : cq[5];
       double gb[6], gt[6], dgb[6], dgt[6];
-#ifndef FO_Q_UNSCALED
       const double qu6 = Qu(q), qv6 = Qv(q), qu4 = 4.0 * qu6, qv4 = 4.0 * qv6;
       (void)rho_a;
-#endif
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-#ifndef FO_Q_UNSCALED
         const double qu = j == a ? qu4 : qu6, qv = j == a ? qv4 : qv6;
-#else
-        const double rj = ((j == a) ? kTwoThirds : kSixth) * rho_a;
-        const double qu = rj * Qu(q), qv = rj * Qv(q);
-#endif
         const double pu = fma(E1x(q), w.a[j], E1y(q) * w.b[j]);
         const double pv = fma(E2x(q), w.a[j], E2y(q) * w.b[j]);
         gb[2 * j] = fma(f0, pu, -qu);
