@@ -175,6 +175,15 @@ FO_API fo_status fo_plan_check_host(int64_t n_vert, const double* xy, int64_t n_
                                     int32_t n_layers, const int32_t* part_of_tri, int32_t my_part,
                                     int32_t n_parts, int64_t* stats);
 
+/* The same host-only check for the quadrilateral footprint of a hexahedral
+ * mesh (fo_mesh_create_quad, NEXT-f4): the quad-patch plan of KH-patch, every
+ * element entry (q, j, j2) of the 4 x 4 corner pairs gathered exactly once,
+ * every slot / residual written once or RED onto a zero fill, the zero
+ * fill's lead / wait lists consistent.  stats[8] as fo_plan_check_host
+ * (contributions: 16 corner pairs per quad). */
+FO_API fo_status fo_plan_check_quad_host(int64_t n_vert, const double* xy, int64_t n_quad, const int32_t* quad,
+                                         int32_t n_layers, int64_t* stats);
+
 /* R = F(U): overwrites d_R[n_dofs].  d_U[n_dofs] fp64. */
 FO_API fo_status fo_assemble_residual(fo_mesh m, const double* d_U, double* d_R, void* stream);
 

@@ -644,7 +644,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
 fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, int64_t n_quad,
                           const int32_t* quad, int32_t L, const double* sigma, const double* thickness,
                           const double* surface, const double* bed, const double* beta, const double* A_elem,
-                          int device, fo_mesh* out) {
+                          int device, fo_mesh* out, bool host_only = false) {
   auto bad = [](fo_status st, const std::string& msg) { set_error(msg); return st; };
   if (!out || !p) return bad(FO_EINVAL, "NULL argument");
   *out = nullptr;
@@ -673,14 +673,17 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
     if (!used[size_t(c)]) return bad(FO_EMESH, "vertex in no quad");
     if (!(thickness[c] >= p->H_min)) return bad(FO_EMESH, "thickness below H_min");
   }
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-    cudaGetLastError();
-    return bad(FO_ECUDA, "no CUDA device available (libfo has no CPU path)");
+  fo_status st = FO_OK;
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      return bad(FO_ECUDA, "no CUDA device available (libfo has no CPU path)");
+    }
+    if (device < 0 || device >= ndev) return bad(FO_EINVAL, "bad device ordinal");
+    st = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+    if (st) return st;
   }
-  if (device < 0 || device >= ndev) return bad(FO_EINVAL, "bad device ordinal");
-  fo_status st = cuda_status(cudaSetDevice(device), "cudaSetDevice");
-  if (st) return st;
 
   // quads in Hilbert order of their centroids (the patch kernel's patches are
   // runs of consecutive quads, so they come out compact); `order[t]` = the
@@ -803,6 +806,12 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
     std::vector<int64_t> pos(m->hex_color_ptr.begin(), m->hex_color_ptr.end() - 1);
     for (int64_t t = 0; t < n_quad; ++t) ids[size_t(pos[size_t(color[size_t(t)])]++)] = int32_t(t);
   }
+  if (host_only) {   // the patch plan only, nothing on a device (fo_plan_check_quad_host)
+    st = build_patch_plan(m, false);
+    if (st) { delete m; return st; }
+    *out = m;
+    return FO_OK;
+  }
   auto up = [](void** dst, const void* src, size_t bytes) {
     if (bytes == 0) return FO_OK;
     fo_status s = cuda_status(cudaMalloc(dst, bytes), "cudaMalloc");
@@ -918,6 +927,21 @@ fo_status launch_hex(fo_mesh m, const double* d_U, double* d_R, double* d_vals, 
 using namespace fo;
 
 extern "C" {
+
+fo_status fo_plan_check_quad_host(int64_t n_vert, const double* xy, int64_t n_quad, const int32_t* quad,
+                                  int32_t n_layers, int64_t* stats) {
+  if (!stats) { set_error("stats is NULL"); return FO_EINVAL; }
+  fo_params p;
+  fo_params_default(&p);
+  std::vector<double> H(size_t(n_vert), 1000.0), srf(size_t(n_vert), 1000.0), beta(size_t(n_vert), 1.0);
+  fo_mesh m = nullptr;
+  fo_status st = hex_create_impl(&p, n_vert, xy, n_quad, quad, n_layers, nullptr, H.data(), srf.data(), nullptr,
+                                 beta.data(), nullptr, 0, &m, true);
+  if (st) return st;
+  st = plan_check(m, stats);
+  delete m;
+  return st;
+}
 
 fo_status fo_mesh_create_quad(const fo_params* p, int64_t n_vert, const double* xy, int64_t n_quad,
                               const int32_t* quad, int32_t n_layers, const double* sigma,

@@ -81,6 +81,7 @@ _SIGS = {
     "fo_halo_plan_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P],
     "fo_part_graph_host": [I64, I64, P, I32, P, I32, I32, P, P, P, P, P, P, P],
     "fo_plan_check_host": [I64, P, I64, P, I32, P, I32, I32, P],
+    "fo_plan_check_quad_host": [I64, P, I64, P, I32, P],
 }
 _VOID = ["fo_mesh_destroy", "fo_graph_destroy", "fo_halo_destroy"]
 
@@ -169,6 +170,18 @@ def plan_check_host(xy, tri, n_layers, part=None, n_parts=1, my_part=0):
     pt = None if part is None else np.ascontiguousarray(part, dtype=np.int32)
     check(lib().fo_plan_check_host(xy.shape[0], _ptr(xy), tri.shape[0], _ptr(tri), n_layers, _ptr(pt),
                                    my_part, n_parts, _ptr(st)), "fo_plan_check_host")
+    keys = ["patches", "pairs", "contributions", "zero_cols", "multi", "bad_slots", "bad_entries", "plan_bytes"]
+    return dict(zip(keys, st.tolist()))
+
+
+def plan_check_quad_host(xy, quad, n_layers):
+    """host-only coverage check of the hexahedral (quad-patch) plan: dict as
+    plan_check_host."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    quad = np.ascontiguousarray(quad, dtype=np.int32)
+    st = np.zeros(8, dtype=np.int64)
+    check(lib().fo_plan_check_quad_host(xy.shape[0], _ptr(xy), quad.shape[0], _ptr(quad), n_layers, _ptr(st)),
+          "fo_plan_check_quad_host")
     keys = ["patches", "pairs", "contributions", "zero_cols", "multi", "bad_slots", "bad_entries", "plan_bytes"]
     return dict(zip(keys, st.tolist()))
 

@@ -68,3 +68,19 @@ def test_patch_classes_match_the_plan(case):
     npatch = _patch_classes(fp)
     for got, want in ((int((npatch >= 2).sum()), st["zero_cols"]), (int((npatch >= 3).sum()), st["multi"])):
         assert want * 0.995 <= got <= want
+
+
+@pytest.mark.parametrize("case", ["C1-quads", "quads-40x40", "quads-33x33-distorted", "quads-700x700"])
+def test_quad_plan_covers_every_entry_once(case):
+    """NEXT-f4 hexahedra: the quad-patch plan of KH-patch (fo_plan_check_quad_host,
+    no device) gathers each of the 16 corner-pair entries of every quad once and
+    writes every slot / residual once (store, RED onto a zero fill, or multi
+    fix-up); 700 x 700 is the timed mesh (~5 100 patches of <= 96 quads)."""
+    fp = {"C1-quads": lambda: mg.to_quads(mg.ismip_hom_a(nx=10, n_layers=5), 10),
+          "quads-40x40": lambda: mg.to_quads(mg.ismip_hom_a(nx=40, n_layers=3), 40),
+          "quads-33x33-distorted": lambda: mg.to_quads(mg.slab(nx=33, n_layers=2, distort=0.2), 33),
+          "quads-700x700": lambda: mg.to_quads(mg.ismip_hom_a(nx=700, n_layers=10), 700)}[case]()
+    st = fo.plan_check_quad_host(fp.xy, fp.tri, fp.n_layers)
+    assert st["bad_slots"] == 0 and st["bad_entries"] == 0, st
+    assert st["contributions"] == 16 * fp.tri.shape[0]
+    assert st["patches"] >= (fp.tri.shape[0] + 95) // 96
