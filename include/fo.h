@@ -189,7 +189,10 @@ FO_API fo_status fo_assemble_residual(fo_mesh m, const double* d_U, double* d_R,
 
 /* vals = dF/dU in the CSR order of g (overwritten); d_R (nullable) = F(U)
  * overwritten in the same pass.  The kernel computes CSR
- * positions from the column structure; it does not read col_idx. */
+ * positions from the column structure; it does not read col_idx.
+ * Assembly calls on ONE mesh must be ordered (one stream, or synchronised):
+ * the mesh owns their scratch (multi-column partial sums, the in-kernel zero
+ * fill's flags and patch ticket).  Different meshes may run concurrently. */
 FO_API fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, double* d_R,
                                double* d_vals, void* stream);
 
