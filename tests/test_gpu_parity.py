@@ -527,3 +527,26 @@ def test_assembly_captures_into_a_cuda_graph(torch_cuda):
     torch.cuda.synchronize()
     assert torch.equal(Rg, R2) and torch.equal(Vg, V2)
     assert not torch.equal(R2, R)
+
+
+def test_hexahedra_full_size_sampled(torch_cuda, ora_mod):
+    """NEXT-f4 at the timed size: 700 x 700 quads x 10 layers (4.9 M
+    hexahedra, ~5 100 quad patches) through the quad-patch kernel; complete rows
+    of 40 random columns (about 40 % of all columns are patch-boundary columns)
+    and of the domain's corner / edge columns vs the oracle on the
+    sub-footprint of their quad fans."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    nx = 700
+    fp = mg.to_quads(mg.ismip_hom_a(nx=nx, n_layers=10), nx)
+    mesh = fo.Mesh.from_footprint(fp)
+    U = torch.tensor(fp.U, device="cuda")
+    g = mesh.graph()
+    R, vals = mesh.jacobian(U)
+    torch.cuda.synchronize()
+    rp, _ = g.to_host()
+    rng = mg.SplitMix64(123)
+    n1 = nx + 1
+    special = np.array([0, nx, nx * n1, n1 * n1 - 1, n1 // 2, (nx // 2) * n1 + nx // 2])
+    cols = np.unique(np.concatenate([(rng.uniform(40) * fp.n_vert).astype(np.int64), special]))
+    _check_full_size_columns(ora_mod, fp, cols, rp, vals.cpu().numpy(), (R.cpu().numpy(),))
