@@ -4,11 +4,13 @@ memcheck, racecheck, synccheck and initcheck.
 
   python tools/sanitize_driver.py C1|C2
 
-Kernels exercised: ka_patch_kernel (R + J and residual-only instances, wedge,
-n = 3 and generic n, tetrahedral), zero_boundary_kernel, multi_fixup_kernel,
-lateral_kernel, the atomic ablation, the hexahedral kernel, the halo gather /
-unpack-add kernels (loopback transport) and the Newton-consumer kernels
-(SpMV, line factor / solve, Krylov dots / update).
+Kernels exercised: ka_ws_kernel (wedge and tetrahedral R + J, with the
+in-kernel zero fill and, through the fused halo call, without), ka_patch_kernel
+(residual-only instances, generic n, the round-1 R + J kernel),
+zero_boundary_kernel, multi_fixup_kernel, lateral_kernel, the atomic
+ablation, the quad-patch and coloured hexahedral kernels, the halo gather /
+unpack-add kernels (loopback transport, sequential and fused) and the
+Newton-consumer kernels (SpMV, line factor / solve, Krylov dots / update).
 """
 import os
 import sys
@@ -64,8 +66,14 @@ def main(cfg):
     # hexahedra
     fq = mg.to_quads(mg.slab(nx=10, n_layers=3, distort=0.1), 10)
     mq = fo.Mesh.from_footprint(fq)
-    mq.jacobian(torch.tensor(fq.U, device=dev))
-    mq.residual(torch.tensor(fq.U, device=dev))
+    mq.jacobian(torch.tensor(fq.U, device=dev))     # quad-patch kernel (KH-patch) + zero fill + fix-up
+    mq.residual(torch.tensor(fq.U, device=dev))     # coloured kernel, residual
+    mq.set_scatter(fo.SCATTER_ATOMIC)
+    mq.jacobian(torch.tensor(fq.U, device=dev))     # coloured R + J ablation
+    # the round-1 single-warpgroup wedge kernel (R + J)
+    m.set_scatter(fo.SCATTER_OWNER_1WG)
+    m.jacobian(U)
+    m.set_scatter(fo.SCATTER_OWNER)
     # halo kernels over the loopback transport (3 parts)
     part = fo.partition(fp.n_tri, 3)
     parts = [fo.Mesh.from_footprint(fp, part=part, my_part=p, n_parts=3) for p in range(3)]
@@ -78,6 +86,11 @@ def main(cfg):
     outs = [pm.jacobian(Ul) for pm, Ul in zip(parts, Us)]
     for hh, (Rp, Vp) in zip(halos, outs):
         hh.sum(Rp, Vp)
+    # fused assembly + export (side stream, split launches, zero kernel)
+    for hh, Ul, (Rp, Vp) in zip(halos, Us, outs):
+        hh.assemble(Ul, Rp, Vp)
+    for hh, Ul, (Rp, Vp) in zip(halos, Us, outs):
+        hh.assemble(Ul, Rp)
     torch.cuda.synchronize()
     assert np.isfinite(R.cpu().numpy()).all() and np.isfinite(V.cpu().numpy()).all()
     print(f"sanitize_driver {cfg} done", flush=True)
