@@ -702,6 +702,8 @@ def main():
             "per_gpu": {"value": value / world, "unit": "Melem/s per GPU",
                         "note": "the metric's per-GPU figure (value = whole job over all GPUs)"},
             "scaling_efficiency": eta, "loopback": loop,
+            "build": {"src_hash": kernel_src_hash(), "extra_nvcc_flags": os.environ.get("FO_EXTRA_NVCC_FLAGS", ""),
+                      "seed": "meshgen SplitMix64 defaults (C3 seed 1, C5 seed 2)"},
             "config": {"workload": f"{cfg_name}: {fp.name}, {fp.n_tri} triangles x {L} layers = "
                                    f"{fp.n_elem} wedges, {world} part(s)",
                        "wedges_per_gpu": mesh.n_elems, "nnz_per_gpu": graph.nnz, "n_dofs_per_gpu": mesh.n_dofs,

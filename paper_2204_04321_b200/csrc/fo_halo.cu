@@ -512,6 +512,7 @@ fo_status fo_halo_create_loopback(const fo_mesh* parts, const fo_graph* graphs, 
 }
 
 fo_status fo_halo_import(fo_halo h, double* d_U, void* stream) {
+  NvtxRange nvtx("fo_halo_import");
   if (!h) return fail(FO_EINVAL, "halo is NULL");
   if (h->n_ranks == 1) return FO_OK;
   if (!d_U) return fail(FO_EINVAL, "d_U is NULL");
@@ -532,6 +533,7 @@ fo_status fo_halo_import(fo_halo h, double* d_U, void* stream) {
 }
 
 fo_status fo_halo_sum(fo_halo h, double* d_R, double* d_vals, void* stream) {
+  NvtxRange nvtx("fo_halo_sum");
   if (!h) return fail(FO_EINVAL, "halo is NULL");
   if (h->n_ranks == 1) return FO_OK;
   fo_status st = cuda_status(cudaSetDevice(h->device), "cudaSetDevice");
@@ -542,6 +544,7 @@ fo_status fo_halo_sum(fo_halo h, double* d_R, double* d_vals, void* stream) {
 
 fo_status fo_assemble_jacobian_halo(fo_mesh m, fo_graph g, fo_halo h, const double* d_U, double* d_R,
                                     double* d_vals, void* stream) {
+  NvtxRange nvtx("fo_assemble_jacobian_halo");
   if (!m || !h) return fail(FO_EINVAL, "mesh or halo is NULL");
   if (!d_U || !d_R) return fail(FO_EINVAL, "d_U or d_R is NULL");
   if (d_vals && (!g || g->mesh != m)) return fail(FO_ESTATE, "graph is NULL or was built for another mesh");

@@ -581,6 +581,7 @@ fo_status fo_graph_to_host(fo_graph g, int64_t* row_ptr, int32_t* col_idx) {
 }
 
 fo_status fo_assemble_residual(fo_mesh m, const double* d_U, double* d_R, void* stream) {
+  NvtxRange nvtx("fo_assemble_residual");
   if (!m) return fail(FO_EINVAL, "mesh is NULL");
   if (m->n_dof > 0 && (!d_U || !d_R)) return fail(FO_EINVAL, "NULL device buffer");
   return launch_residual(m, d_U, d_R, stream);
@@ -588,6 +589,7 @@ fo_status fo_assemble_residual(fo_mesh m, const double* d_U, double* d_R, void* 
 
 fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, double* d_R,
                                double* d_vals, void* stream) {
+  NvtxRange nvtx("fo_assemble_jacobian");
   if (!m || !g) return fail(FO_EINVAL, "mesh or graph is NULL");
   if (g->mesh != m) return fail(FO_ESTATE, "graph was built for another mesh");
   if (m->n_dof > 0 && (!d_U || !d_vals)) return fail(FO_EINVAL, "NULL device buffer");
@@ -596,6 +598,7 @@ fo_status fo_assemble_jacobian(fo_mesh m, fo_graph g, const double* d_U, double*
 
 fo_status fo_assemble_jacobian_host(fo_mesh m, fo_graph g, const double* h_U, double* h_R,
                                     double* h_vals, void* stream) {
+  NvtxRange nvtx("fo_assemble_jacobian_host");
   if (!m || !g) return fail(FO_EINVAL, "mesh or graph is NULL");
   if (g->mesh != m) return fail(FO_ESTATE, "graph was built for another mesh");
   if (m->n_dof > 0 && (!h_U || !h_vals)) return fail(FO_EINVAL, "NULL host buffer");

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges cost nothing without a profiler attached
+
 #include "../../include/fo.h"
 
 namespace fo {
@@ -235,6 +237,14 @@ struct fo_graph_s {
 };
 
 namespace fo {
+// NVTX range over one public call (nsys / ncu --nvtx-include):
+// fo_assemble_*, fo_halo_import / fo_halo_sum
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 // Local topology of one footprint part (fo_host.cpp build_topology).
 struct Topo {
   int64_t nA = 0, nB = 0, nC = 0;
