@@ -550,3 +550,30 @@ def test_hexahedra_full_size_sampled(torch_cuda, ora_mod):
     special = np.array([0, nx, nx * n1, n1 * n1 - 1, n1 // 2, (nx // 2) * n1 + nx // 2])
     cols = np.unique(np.concatenate([(rng.uniform(40) * fp.n_vert).astype(np.int64), special]))
     _check_full_size_columns(ora_mod, fp, cols, rp, vals.cpu().numpy(), (R.cpu().numpy(),))
+
+
+def test_c3_repeated_assemblies_bitwise_on_device(torch_cuda):
+    """Stress of the in-kernel zero fill (atomic patch tickets, lead flags,
+    waits) and of the boundary REDs: 50 back-to-back C3 R + J assemblies into
+    the same buffers, each compared bit for bit with the first on the device;
+    the values are poisoned with NaN between calls, so a slot the zero fill or
+    the stores missed would show."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.greenland_like_1_10()
+    mesh = fo.Mesh.from_footprint(fp)
+    g = mesh.graph()
+    U = torch.tensor(fp.U, device="cuda")
+    R = torch.empty(mesh.n_dofs, dtype=torch.float64, device="cuda")
+    V = torch.empty(g.nnz, dtype=torch.float64, device="cuda")
+    mesh.jacobian(U, g, R, V)
+    R0, V0 = R.clone(), V.clone()
+    assert not torch.isnan(V0).any() and not torch.isnan(R0).any()
+    bad = 0
+    for _ in range(50):
+        R.fill_(float("nan"))
+        V.fill_(float("nan"))
+        mesh.jacobian(U, g, R, V)
+        bad += int(not torch.equal(V, V0)) + int(not torch.equal(R, R0))
+    torch.cuda.synchronize()
+    assert bad == 0
