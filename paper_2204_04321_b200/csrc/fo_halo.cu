@@ -9,6 +9,7 @@
 // contiguous slice of its R and CSR values (zero-copy sends).  The owner adds
 // the received slices into its owned rows with a precomputed position map,
 // one sender at a time in ascending rank order (deterministic).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -401,6 +402,24 @@ fo_status halo_plan(fo_halo h, fo_mesh local) {
   }
   return st;
 }
+// cuStreamWaitValue32 from the driver (no libcuda link): the side stream
+// waits on the kernel's ready flag
+typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValueFn>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
 fo_status halo_streams(fo_halo h) {
   int lo = 0, hi = 0;
   fo_status st = cuda_status(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
@@ -560,11 +579,24 @@ fo_status fo_assemble_jacobian_halo(fo_mesh m, fo_graph g, fo_halo h, const doub
     if (!st && h->n_ranks > 1) st = halo_sum_impl(h, d_R, d_vals, s, s);
     return st;
   }
-  st = launch_owner_overlap(m, d_U, d_R, d_vals, s, h->side, h->ev0, h->ev_b);
-  if (st) return st;
-  // the ghost rows are final on `side` (ev_b): send them while the interior
-  // patches run on s; the unpack-add joins s after both
-  return halo_sum_impl(h, d_R, d_vals, h->side, s);
+  WaitValueFn wv = wait_value_fn();
+  if (wv) {
+    st = launch_owner_overlap(m, d_U, d_R, d_vals, s, h->side, h->ev0,
+                              [wv](cudaStream_t side, const int32_t* flag) -> fo_status {
+                                const CUresult r = wv(reinterpret_cast<CUstream>(side),
+                                                      reinterpret_cast<CUdeviceptr>(flag), 1,
+                                                      CU_STREAM_WAIT_VALUE_GEQ);
+                                return r == CUDA_SUCCESS ? FO_OK : fail(FO_ECUDA, "cuStreamWaitValue32 failed");
+                              });
+    // the side stream sends the ghost rows once the boundary patches raised
+    // the ready flag, while the interior patches run on s; the unpack-add
+    // joins s after both
+    if (st == FO_OK) return halo_sum_impl(h, d_R, d_vals, h->side, s);
+    if (st != FO_ESTATE) return st;
+  }
+  // no overlap available: the sequential order
+  st = d_vals ? launch_jacobian(m, d_U, d_R, d_vals, s) : launch_residual(m, d_U, d_R, s);
+  return st ? st : halo_sum_impl(h, d_R, d_vals, s, s);
 }
 
 fo_status fo_halo_info(fo_halo h, int32_t* n_neighbors, int64_t* recv_rows, int64_t* recv_vals) {

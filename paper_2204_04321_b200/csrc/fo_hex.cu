@@ -847,7 +847,7 @@ static fo_status launch_hex_owner(fo_mesh m, const double* d_U, double* R, doubl
   const KParams kp = make_kparams(m);
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
               m->d_plan.blob_off, m->d_plan.partials, 0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
-              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches};
+              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches, m->d_plan.multi, 0, 0, 0};
   const size_t sm = size_t(d_vals ? kPlanOffsetQ : kPlanOffsetQR) + kPlanBytesHex;
   auto go = [&](auto kern) -> fo_status {
     fo_status e = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <vector_types.h>
 #include <cuda_runtime.h>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -272,7 +273,8 @@ fo_status build_patch_plan(fo_mesh m, bool upload = true);
 fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
 fo_status launch_owner_fixup(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
 fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
-                               cudaStream_t side, cudaEvent_t ev0, cudaEvent_t ev_b);
+                               cudaStream_t side, cudaEvent_t ev0,
+                               const std::function<fo_status(cudaStream_t, const int32_t*)>& wait_ready);
 void free_patch_plan(fo_mesh m);
 fo_status plan_check(const fo_mesh m, int64_t* stats);
 // NEXT-f1 lateral margin term (fo_lateral.cu)

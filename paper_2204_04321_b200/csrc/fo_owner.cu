@@ -25,6 +25,7 @@
 #include "fo_element_tet.cuh"
 #include "fo_element_ws.cuh"
 
+#include <functional>
 #include <type_traits>
 #include "fo_internal.h"
 #include "fo_kernels.cuh"
@@ -315,6 +316,49 @@ ka_patch_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   phase_b<NEED_J>(sp, L, L, D, O, R, vals, pv.partials, threadIdx.x, blockDim.x);
 }
 
+// multi columns: add the patches' partial blocks in patch order and store the
+// self-slot entries and the residual; item i = (record i / (L+1), row level)
+__device__ __forceinline__ void multi_fixup_one(const MultiRec* __restrict__ mr, int i, int L,
+                                                const double* __restrict__ partials, double* __restrict__ R,
+                                                double* __restrict__ vals) {
+  const int mc = i / (L + 1), kk = i - mc * (L + 1);
+  const MultiRec r = mr[mc];
+  const bool up = vals && kk < L;
+  double s[14];
+#pragma unroll
+  for (int e = 0; e < 14; ++e) s[e] = 0.0;
+  for (int b = 0; b < r.cnt; ++b) {
+    const double* q = partials + (int64_t(r.base + b) * (L + 1) + kk) * kPartialStride;
+    s[12] += q[12];
+    s[13] += q[13];
+    if (vals) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[e] += q[e];
+    }
+    if (up) {
+#pragma unroll
+      for (int e = 4; e < 12; ++e) s[e] += q[e];
+    }
+  }
+  *reinterpret_cast<double2*>(R + 2 * (int64_t(r.c) * (L + 1) + kk)) = make_double2(s[12], s[13]);
+  if (!vals) return;
+  const int nc = r.nc_self & 255, slot = r.nc_self >> 8;
+  const int m0 = (kk == 0 || kk == L) ? 2 : 3, m1 = (kk + 1 == L) ? 2 : 3;
+  const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
+  const int g0 = kk == 0 ? 0 : 2;
+  double* d0 = vals + r.colstart + int64_t(4 * nc) * P0 + int64_t(slot) * (2 * m0) + g0;
+  double* d1 = d0 + 2 * nc * m0;
+  *reinterpret_cast<double2*>(d0) = make_double2(s[0], s[1]);
+  *reinterpret_cast<double2*>(d1) = make_double2(s[2], s[3]);
+  if (up) {
+    *reinterpret_cast<double2*>(d0 + 2) = make_double2(s[4], s[5]);
+    *reinterpret_cast<double2*>(d1 + 2) = make_double2(s[6], s[7]);
+    double* e0 = vals + r.colstart + int64_t(4 * nc) * P1 + int64_t(slot) * (2 * m1);
+    *reinterpret_cast<double2*>(e0) = make_double2(s[8], s[9]);
+    *reinterpret_cast<double2*>(e0 + 2 * nc * m1) = make_double2(s[10], s[11]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // KA-ws: the warp-specialised patch kernel ("KA-ws").
 // Same patch plan, shared layout and scatter (phase B) as ka_patch_kernel, but
@@ -363,6 +407,7 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
   __shared__ uint64_t plan_bar;
   __shared__ uint32_t tmem_base;
   __shared__ int ticket;
+  __shared__ int last_bnd;
   if (pv.inkz && threadIdx.x == 0) ticket = atomicAdd(pv.flags + pv.n_patches, 1);
   __syncthreads();
   // with the in-kernel zero fill a CTA's patch is its ticket: a lead patch
@@ -527,6 +572,26 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       phase_b<true>(sp, kk, L, D, O, R, vals, pv.partials, tb, kWsHalf);
       if (kk < L) named_arrive(kBarEmpty, kWsThreads);
     }
+    if (pv.trig && p < pv.n_bnd) {
+      // fused halo: count the finished boundary patches; the last one runs the
+      // fix-up of the multi columns only they touch and raises the ready flag
+      named_sync(kBarScat, kWsHalf);
+      if (tb == 0) {
+        __threadfence();   // this patch's stores (ordered by the barrier) before the count
+        last_bnd = atomicAdd(pv.flags + pv.n_patches + 1, 1) == pv.n_bnd - 1;
+        __threadfence();   // and every other boundary patch's before the fix-up reads
+      }
+      named_sync(kBarScat, kWsHalf);
+      if (last_bnd) {
+        for (int i = tb; i < pv.n_multi_bnd * (L + 1); i += kWsHalf)
+          multi_fixup_one(pv.multi, i, L, pv.partials, R, vals);
+        named_sync(kBarScat, kWsHalf);
+        if (tb == 0) {
+          __threadfence();
+          asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(pv.flags + pv.n_patches + 2), "r"(1) : "memory");
+        }
+      }
+    }
   }
 }
 
@@ -555,57 +620,22 @@ __global__ void multi_fixup_kernel(const MultiRec* __restrict__ mr, int n, int L
                                    const double* __restrict__ partials, double* __restrict__ R,
                                    double* __restrict__ vals) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n * (L + 1)) return;
-  const int mc = i / (L + 1), kk = i - mc * (L + 1);
-  const MultiRec r = mr[mc];
-  const bool up = vals && kk < L;
-  double s[14];
-#pragma unroll
-  for (int e = 0; e < 14; ++e) s[e] = 0.0;
-  for (int b = 0; b < r.cnt; ++b) {
-    const double* q = partials + (int64_t(r.base + b) * (L + 1) + kk) * kPartialStride;
-    s[12] += q[12];
-    s[13] += q[13];
-    if (vals) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) s[e] += q[e];
-    }
-    if (up) {
-#pragma unroll
-      for (int e = 4; e < 12; ++e) s[e] += q[e];
-    }
-  }
-  *reinterpret_cast<double2*>(R + 2 * (int64_t(r.c) * (L + 1) + kk)) = make_double2(s[12], s[13]);
-  if (!vals) return;
-  const int nc = r.nc_self & 255, slot = r.nc_self >> 8;
-  const int m0 = (kk == 0 || kk == L) ? 2 : 3, m1 = (kk + 1 == L) ? 2 : 3;
-  const int P0 = kk == 0 ? 0 : 3 * kk - 1, P1 = 3 * kk + 2;
-  const int g0 = kk == 0 ? 0 : 2;
-  double* d0 = vals + r.colstart + int64_t(4 * nc) * P0 + int64_t(slot) * (2 * m0) + g0;
-  double* d1 = d0 + 2 * nc * m0;
-  *reinterpret_cast<double2*>(d0) = make_double2(s[0], s[1]);
-  *reinterpret_cast<double2*>(d1) = make_double2(s[2], s[3]);
-  if (up) {
-    *reinterpret_cast<double2*>(d0 + 2) = make_double2(s[4], s[5]);
-    *reinterpret_cast<double2*>(d1 + 2) = make_double2(s[6], s[7]);
-    double* e0 = vals + r.colstart + int64_t(4 * nc) * P1 + int64_t(slot) * (2 * m1);
-    *reinterpret_cast<double2*>(e0) = make_double2(s[8], s[9]);
-    *reinterpret_cast<double2*>(e0 + 2 * nc * m1) = make_double2(s[10], s[11]);
-  }
+  if (i < n * (L + 1)) multi_fixup_one(mr, i, L, partials, R, vals);
 }
 
 static size_t smem_bytes(bool need_j) { return size_t(need_j ? kPlanOffset : kPlanOffsetR) + kPlanBytes; }
 
 template <bool N3, bool TET>
 static fo_status launch_ws(fo_mesh m, const double* U, double* R, double* vals, cudaStream_t s, int p0, int np,
-                           bool inkz) {
+                           bool inkz, bool trig = false) {
   const size_t sm = size_t(kWsSmem);
   fo_status st = cuda_status(cudaFuncSetAttribute(ka_ws_kernel<N3, TET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sm)), "cudaFuncSetAttribute");
   if (st) return st;
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
               m->d_plan.blob_off, m->d_plan.partials, p0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
-              m->d_plan.wl_ptr, m->d_plan.flags, inkz ? 1 : 0, m->plan.n_patches};
+              m->d_plan.wl_ptr, m->d_plan.flags, inkz ? 1 : 0, m->plan.n_patches,
+              m->d_plan.multi, trig ? 1 : 0, m->plan.n_bnd_patches, m->plan.n_multi_bnd};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
@@ -635,7 +665,7 @@ static fo_status launch_patch(fo_mesh m, const double* U, double* R, double* val
   }
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
               m->d_plan.blob_off, m->d_plan.partials, p0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
-              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches};
+              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches, m->d_plan.multi, 0, 0, 0};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     cudaEventCreate(&e0);
@@ -691,7 +721,7 @@ bool uses_ws(const OwnerCall& c) {
 fo_status owner_prologue(OwnerCall& c, cudaStream_t s, bool inkz = false) {
   fo_mesh m = c.m;
   if (inkz) {
-    fo_status st = cuda_status(cudaMemsetAsync(m->d_plan.flags, 0, sizeof(int32_t) * (m->plan.n_patches + 1), s),
+    fo_status st = cuda_status(cudaMemsetAsync(m->d_plan.flags, 0, sizeof(int32_t) * (m->plan.n_patches + 3), s),
                                "cudaMemsetAsync");
     if (st) return st;
   }
@@ -712,17 +742,17 @@ fo_status owner_prologue(OwnerCall& c, cudaStream_t s, bool inkz = false) {
   return FO_OK;
 }
 
-fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1, bool inkz = false) {
+fo_status owner_patches(OwnerCall& c, cudaStream_t s, int p0, int p1, bool inkz = false, bool trig = false) {
   if (p1 <= p0) return FO_OK;
   fo_mesh m = c.m;
   const bool need_j = c.vals != nullptr, n3 = m->p.glen_n == 3.0, tet = m->elem_type == FO_ELEM_TET3;
   const int np = p1 - p0;
   fo_status st;
   if (uses_ws(c))
-    st = tet ? (n3 ? launch_ws<true, true>(m, c.U, c.R, c.vals, s, p0, np, inkz)
-                   : launch_ws<false, true>(m, c.U, c.R, c.vals, s, p0, np, inkz))
-             : (n3 ? launch_ws<true, false>(m, c.U, c.R, c.vals, s, p0, np, inkz)
-                   : launch_ws<false, false>(m, c.U, c.R, c.vals, s, p0, np, inkz));
+    st = tet ? (n3 ? launch_ws<true, true>(m, c.U, c.R, c.vals, s, p0, np, inkz, trig)
+                   : launch_ws<false, true>(m, c.U, c.R, c.vals, s, p0, np, inkz, trig))
+             : (n3 ? launch_ws<true, false>(m, c.U, c.R, c.vals, s, p0, np, inkz, trig)
+                   : launch_ws<false, false>(m, c.U, c.R, c.vals, s, p0, np, inkz, trig));
   else if (need_j)
     st = tet ? (n3 ? launch_patch<true, true, true>(m, c.U, c.R, c.vals, s, p0, np)
                    : launch_patch<true, false, true>(m, c.U, c.R, c.vals, s, p0, np))
@@ -786,26 +816,30 @@ fo_status launch_owner(fo_mesh m, const double* d_U, double* d_R, double* d_vals
   return FO_OK;
 }
 
-// Boundary-first assembly of a part mesh (fo_assemble_jacobian_halo): the
-// patches holding every ghost-touching triangle and the fix-up of the multi
-// columns they alone touch run on `side` (a higher-priority stream), the
-// interior patches on `s` at the same time; `ev_b` is recorded on `side` once
-// the ghost rows are final, so the halo sum can send them while the interior
-// patches are still running.  On return `s` has joined `side` for the
-// remaining fix-up; everything after it (lateral term, unpack-add) goes on s.
+// Boundary-first assembly of a part mesh with the ghost-row sum overlapped
+// (fo_assemble_jacobian_halo): ONE warp-specialised launch over all patches
+// with the in-kernel zero fill; a part mesh orders its ghost-touching
+// triangles first, so the boundary patches draw tickets 0 .. K-1, and the
+// last of them to finish runs the fix-up of the multi columns only they touch
+// and raises the ready flag.  The halo's side stream waits for that flag
+// (stream memory operation `wait_value`) and sends the final ghost rows while
+// the interior patches are still running; the remaining fix-up follows the
+// kernel on `s`.  Returns FO_ESTATE when this path does not apply (not the
+// warp-specialised kernel, or no boundary patches): the caller then runs the
+// sequential order.
 fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
-                               cudaStream_t side, cudaEvent_t ev0, cudaEvent_t ev_b) {
+                               cudaStream_t side, cudaEvent_t ev0, const std::function<fo_status(
+                                   cudaStream_t, const int32_t*)>& wait_ready) {
   OwnerCall c;
   fo_status st = owner_begin(c, m, d_U, d_R, d_vals);
-  if (!st) st = owner_prologue(c, s);
+  if (st) return st;
+  const int K = m->plan.n_bnd_patches, nmb = m->plan.n_multi_bnd;
+  if (!uses_ws(c) || K == 0) return FO_ESTATE;
+  st = owner_prologue(c, s, true);
   if (!st) st = cuda_status(cudaEventRecord(ev0, s), "cudaEventRecord");
   if (!st) st = cuda_status(cudaStreamWaitEvent(side, ev0, 0), "cudaStreamWaitEvent");
-  const int K = m->plan.n_bnd_patches, nmb = m->plan.n_multi_bnd;
-  if (!st) st = owner_patches(c, side, 0, K);
-  if (!st) st = owner_multi(c, side, 0, nmb);
-  if (!st) st = cuda_status(cudaEventRecord(ev_b, side), "cudaEventRecord");
-  if (!st) st = owner_patches(c, s, K, m->plan.n_patches);
-  if (!st) st = cuda_status(cudaStreamWaitEvent(s, ev_b, 0), "cudaStreamWaitEvent");
+  if (!st) st = wait_ready(side, m->d_plan.flags + m->plan.n_patches + 2);
+  if (!st) st = owner_patches(c, s, 0, m->plan.n_patches, true, true);
   if (!st) st = owner_multi(c, s, nmb, int(m->plan.multi.size()));
   if (st) return st;
   m->last_launches = c.launches;

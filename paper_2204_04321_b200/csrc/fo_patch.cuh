@@ -27,9 +27,15 @@ struct PlanView {
   const int32_t* __restrict__ zl_ptr;
   const int32_t* __restrict__ wl;
   const int32_t* __restrict__ wl_ptr;
-  int32_t* flags;
+  int32_t* flags;     // [n_patches + 3]: per-patch zero-fill flags | ticket | boundary-done count | ready
   int inkz;
   int n_patches;
+  // fused halo (trig != 0, fo_assemble_jacobian_halo): the last of the n_bnd
+  // boundary patches (tickets 0 .. n_bnd-1) runs the fix-up of the multi
+  // records 0 .. n_multi_bnd-1 and raises flags[n_patches + 2], which the
+  // halo's side stream waits on before sending the ghost rows
+  const MultiRec* __restrict__ multi;
+  int trig, n_bnd, n_multi_bnd;
 };
 
 // one-shot bulk copy global -> shared with an mbarrier (TMA, non-tensor):

@@ -333,7 +333,7 @@ fo_status build_patch_plan(fo_mesh m, bool upload) {
   if (!st) st = upload_vec(&m->d_plan.wl, P.wl);
   if (!st) st = upload_vec(&m->d_plan.wl_ptr, P.wl_ptr);
   if (!st)
-    st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.flags), sizeof(int32_t) * (P.n_patches + 1)),
+    st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.flags), sizeof(int32_t) * (P.n_patches + 3)),
                      "cudaMalloc");
   if (!st && P.n_partials > 0)
     st = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_plan.partials),

@@ -47,7 +47,7 @@ def line(name, ms, note):
 
 
 jac = lambda: mesh.jacobian(U, g, R, V)
-line("base", timeit(jac), "R + J, wedges, owner-computes scatter")
+line("base", timeit(jac), "R + J, wedges, warp-specialised owner-computes kernel")
 line("r_only", timeit(lambda: mesh.residual(U, R)), "R only")
 mesh.set_temperature(fp.T_star, fp.arrhenius["A0"], fp.arrhenius["Q"])
 line("f3_temperature", timeit(jac), "R + J, A = A0 exp(-Q/RT*) per wedge in-kernel")
@@ -56,7 +56,7 @@ mesh.set_lateral(True)
 line("f1_lateral", timeit(jac), "R + J + lateral margin term kernel")
 mesh.set_lateral(False)
 mesh.set_element(1)
-line("f4_tet3", timeit(jac), "R + J, three P1 tetrahedra per prism (14.4 M tets)")
+line("f4_tet3", timeit(jac), "R + J, three P1 tetrahedra per prism (14.4 M tets), warp-specialised kernel")
 line("f4_tet3_r_only", timeit(lambda: mesh.residual(U, R)), "R only, tetrahedra")
 
 # hexahedra on a quadrilateral footprint of C3 size (700 x 700 quads x 10 layers)
@@ -69,7 +69,13 @@ Vq = torch.empty(gq.nnz, dtype=torch.float64, device="cuda")
 ms = timeit(lambda: mq.jacobian(Uq, gq, Rq, Vq))
 print(json.dumps({"variant": "f4_hex8", "workload": "700x700 quads x 10 layers", "wedges": fq.n_elem,
                   "ms": round(ms, 4), "Melem_s": round(fq.n_elem / ms / 1e3, 1), "launches": mq.last_launch_count(),
-                  "note": "R + J, 8-node trilinear hexahedra, coloured scatter"}), flush=True)
+                  "note": "R + J, 8-node trilinear hexahedra, quad-patch owner-computes kernel"}), flush=True)
+mq.set_scatter(fo.SCATTER_ATOMIC)
+ms = timeit(lambda: mq.jacobian(Uq, gq, Rq, Vq))
+print(json.dumps({"variant": "f4_hex8_coloured", "workload": "700x700 quads x 10 layers", "wedges": fq.n_elem,
+                  "ms": round(ms, 4), "Melem_s": round(fq.n_elem / ms / 1e3, 1), "launches": mq.last_launch_count(),
+                  "note": "R + J, hexahedra, coloured read-modify-write ablation"}), flush=True)
+mq.set_scatter(fo.SCATTER_OWNER)
 ms = timeit(lambda: mq.residual(Uq, Rq))
 print(json.dumps({"variant": "f4_hex8_r_only", "workload": "700x700 quads x 10 layers", "wedges": fq.n_elem,
                   "ms": round(ms, 4), "Melem_s": round(fq.n_elem / ms / 1e3, 1), "launches": mq.last_launch_count(),
