@@ -326,6 +326,33 @@ def cpu_baseline_oracle(fp, n_tri_sample_per_core, one_core_tris=6000):
             "cpu_model": cpu_model(), "compiler": ORACLE_COMPILER}
 
 
+def small_config_lines(dev, flush, stream):
+    """SURVEY.md 8(d) d5 per config: the small configurations C1 (ISMIP-HOM A,
+    4 000 wedges) and C2 (Greenland-like 16 km, ~300 k wedges) -- one R + J
+    assembly on the GPU (median of 10 after warm-up, CUDA events) and one
+    whole-config oracle evaluation on ONE host core (median of 2 after a warm-up
+    for C1, one evaluation for C2)."""
+    import torch
+    from paper_2204_04321_b200 import fo, meshgen as mg
+    out = {}
+    for name, make, reps in (("C1", mg.ismip_hom_a, 3), ("C2", lambda: mg.greenland_like(16.0), 1)):
+        fpc = make()
+        m = fo.Mesh.from_footprint(fpc, device=dev.index)
+        g = m.graph()
+        U = torch.tensor(fpc.U, device=dev)
+        R = torch.empty(m.n_dofs, dtype=torch.float64, device=dev)
+        V = torch.empty(g.nnz, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            m.jacobian(U, g, R, V)
+        ms = statistics.median(time_steps(lambda: m.jacobian(U, g, R, V), 10, flush, stream))
+        secs, nt, nw = oracle_parallel(fpc, fpc.n_tri, 1, reps=reps)
+        t1 = statistics.median(secs[1:] if reps > 1 else secs)
+        out[name] = {"wedges": fpc.n_elem, "gpu_ms": ms, "gpu_Melem_s": fpc.n_elem / ms / 1e3,
+                     "oracle_1core_s": t1, "oracle_1core_Melem_s": nw / t1 / 1e6}
+        m.close()
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only),
     one process per core on a Hilbert-contiguous split of a bounded sample."""
@@ -689,6 +716,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_oracle(fp, args.cpu_sample_tris)
+        cpu["per_config"] = small_config_lines(dev, flush, stream)
 
     if world > 1:
         dist.barrier()
