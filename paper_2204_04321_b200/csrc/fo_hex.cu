@@ -27,6 +27,7 @@
 #include "fo_internal.h"
 #include "fo_kernels.cuh"
 #include "fo_patch.cuh"
+#include "fo_tmem.cuh"
 
 namespace fo {
 
@@ -156,6 +157,48 @@ __device__ __forceinline__ void hex_basal(const HexIn& h, double (&r)[16], doubl
         }
     }
   }
+}
+
+// the point's strain-rate vectors and viscosity factors as a 7-double record
+// [e1x, exy, exz, e2y, eyz, c, d] (KH-patch keeps it in TMEM for passes 2, 3)
+template <bool N3>
+__device__ __forceinline__ void hex_visc_rec(const HexIn& h, const double G[8][3], double W, const KParams& kp,
+                                             double g[16], double& c, double& d, double rec[7]) {
+  double ux = 0, uy = 0, uz = 0, vx = 0, vy = 0, vz = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ux = fma(h.Uu[i], G[i][0], ux); uy = fma(h.Uu[i], G[i][1], uy); uz = fma(h.Uu[i], G[i][2], uz);
+    vx = fma(h.Uv[i], G[i][0], vx); vy = fma(h.Uv[i], G[i][1], vy); vz = fma(h.Uv[i], G[i][2], vz);
+  }
+  const double exy = 0.5 * (uy + vx), exz = 0.5 * uz, eyz = 0.5 * vz;
+  const double qq = fma(ux, ux, fma(vy, vy, fma(ux, vy, fma(exy, exy, fma(exz, exz, eyz * eyz)))));
+  const double qe = qq + kp.eps;
+  if (N3) {
+    const double y = rcbrt_n3(qe);
+    c = W * h.Afac * y;
+    d = c * (y * y * y) * (1.0 / 3.0);
+  } else {
+    c = W * h.Afac * pow(qe, (1.0 - kp.glen_n) / (2.0 * kp.glen_n));
+    d = c * ((kp.glen_n - 1.0) / (2.0 * kp.glen_n)) / qe;
+  }
+  const double e1x = 2.0 * ux + vy, e2y = ux + 2.0 * vy;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    g[2 * i] = fma(e1x, G[i][0], fma(exy, G[i][1], exz * G[i][2]));
+    g[2 * i + 1] = fma(exy, G[i][0], fma(e2y, G[i][1], eyz * G[i][2]));
+  }
+  rec[0] = e1x; rec[1] = exy; rec[2] = exz; rec[3] = e2y; rec[4] = eyz; rec[5] = c; rec[6] = d;
+}
+// g, c, d from a stored record and the point's gradients
+__device__ __forceinline__ void hex_g_rec(const double G[8][3], const double rec[7], double g[16], double& c,
+                                          double& d) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    g[2 * i] = fma(rec[0], G[i][0], fma(rec[1], G[i][1], rec[2] * G[i][2]));
+    g[2 * i + 1] = fma(rec[1], G[i][0], fma(rec[3], G[i][1], rec[4] * G[i][2]));
+  }
+  c = rec[5];
+  d = rec[6];
 }
 
 // J entry (row dof p, column dof p2) at one point: c H - d g g^T
@@ -407,6 +450,7 @@ __host__ __device__ constexpr int dmap4(int p, int p2) {
              : 4 * ((p >> 1) * (7 - (p >> 1)) / 2 + ((p2 >> 1) - (p >> 1) - 1)) + 2 * (p & 1) + (p2 & 1);
 }
 constexpr int kHexDR = 36;   // residual entries of D: 36 + 2 j + a
+constexpr uint32_t kHexTmCols = 128;   // TMEM per CTA: 8 point records x 7 doubles per thread
 constexpr int kPlanOffsetQ = (kHexDE + kHexOE) * TPQ * 8 / 16 * 16 + 16;
 constexpr int kPlanOffsetQR = kHexDE * TPQ * 8 / 16 * 16 + 16;
 
@@ -498,6 +542,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
   const int p = int(blockIdx.x);
   const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   __shared__ uint64_t plan_bar;
+  __shared__ uint32_t tmem_base;
   SmemPlan sp;
   {
     const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
@@ -510,13 +555,20 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
     sp.ncols = c1 - c0; sp.npairs = q1 - q0;
     sp.nedge = __ldg(pv.nedge + p);
     if (threadIdx.x == 0) bulk_init(&plan_bar);
+    if (NEED_J && threadIdx.x < 32) tmem::alloc(&tmem_base, kHexTmCols);   // warp 0 owns the TMEM
+    tmem::fence_before();
     __syncthreads();
+    tmem::fence_after();
     if (threadIdx.x == 0) bulk_load(base, pv.blob + b0, unsigned(b1 - b0), &plan_bar);
   }
   const int L = kp.L;
   const int tl = threadIdx.x;
   const bool active = tl < nt;
-  const int qi = t0 + (active ? tl : 0);
+  // tcgen05.ld / st are warp-collective: lanes without a quad evaluate a copy
+  // of the patch's last one and publish nothing
+  const bool run = NEED_J ? true : active;
+  const int qi = t0 + (active ? tl : nt - 1);
+  const uint32_t tm = tmem_base + (uint32_t(tl & ~31) << 16);   // this warp's lane quarter
   const QuadRec qr = quads[qi];
   if (active) {
 #pragma unroll
@@ -528,7 +580,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
     for (int i = threadIdx.x; i < kHexOE; i += blockDim.x) O[i * TPQ + kPatchQuads] = 0.0;
   double held[kHexDE];
   for (int k = 0; k < L; ++k) {
-    if (active) {
+    if (run) {
       HexIn h;
       const double s0 = __ldg(sigma + k), s1 = __ldg(sigma + k + 1);
 #pragma unroll
@@ -557,7 +609,13 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int qp = 0; qp < 8; ++qp) {
           double N[8], G[8][3], g[16], c, d;
           const double W = hex_point(h, qp, N, G);
-          hex_visc<N3>(h, G, W, kp, g, c, d);
+          if (NEED_J) {
+            double rec[7];
+            hex_visc_rec<N3>(h, G, W, kp, g, c, d, rec);
+            tmem::st<7>(tm + 14 * qp, rec);
+          } else {
+            hex_visc<N3>(h, G, W, kp, g, c, d);
+          }
           double sx = 0, sy = 0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) { sx = fma(h.S[i & 3], G[i][0], sx); sy = fma(h.S[i & 3], G[i][1], sy); }
@@ -570,18 +628,21 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
           if (NEED_J) hex_accum<0>(G, g, c, d, bb);
         }
         if (k == 0) hex_basal<NEED_J>(h, r, bb);
+        if (active) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) D[(kHexDR + i) * TPQ + tl] += r[i];
+          for (int i = 0; i < 8; ++i) D[(kHexDR + i) * TPQ + tl] += r[i];
+          if (NEED_J) {
+            int e = 0;
+#pragma unroll
+            for (int pp = 0; pp < 8; ++pp)
+#pragma unroll
+              for (int p2 = pp; p2 < 8; ++p2) { D[dmap4(pp, p2) * TPQ + tl] += bb[e]; ++e; }
+          }
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) held[kHexDR + i] = r[8 + i];
-        if (NEED_J) {
-          int e = 0;
-#pragma unroll
-          for (int pp = 0; pp < 8; ++pp)
-#pragma unroll
-            for (int p2 = pp; p2 < 8; ++p2) { D[dmap4(pp, p2) * TPQ + tl] += bb[e]; ++e; }
-        }
       }
+      if (NEED_J) tmem::wait_st();   // the point records are in TMEM
       if (NEED_J) {
         // ---- pass 2: (bottom, top) block -> O
         double bt[64];
@@ -591,11 +652,16 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int qp = 0; qp < 8; ++qp) {
           double N[8], G[8][3], g[16], c, d;
           const double W = hex_point(h, qp, N, G);
-          hex_visc<N3>(h, G, W, kp, g, c, d);
+          (void)W;
+          double rec[7];
+          tmem::ld<7>(tm + 14 * qp, rec);
+          hex_g_rec(G, rec, g, c, d);
           hex_accum<1>(G, g, c, d, bt);
         }
+        if (active) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) O[i * TPQ + tl] = bt[i];
+          for (int i = 0; i < 64; ++i) O[i * TPQ + tl] = bt[i];
+        }
         // ---- pass 3: (top, top) block -> held
         double tt[36];
 #pragma unroll
@@ -604,7 +670,10 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int qp = 0; qp < 8; ++qp) {
           double N[8], G[8][3], g[16], c, d;
           const double W = hex_point(h, qp, N, G);
-          hex_visc<N3>(h, G, W, kp, g, c, d);
+          (void)W;
+          double rec[7];
+          tmem::ld<7>(tm + 14 * qp, rec);
+          hex_g_rec(G, rec, g, c, d);
           hex_accum<2>(G, g, c, d, tt);
         }
         int e = 0;
@@ -635,6 +704,12 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
   __syncthreads();
   if (NEED_J) phase_bq_j<false>(sp, L, L, D, O, vals, pv.partials, threadIdx.x, blockDim.x);
   phase_bq_r(sp, L, L, D + kHexDR * TPQ, R, pv.partials, threadIdx.x, blockDim.x);
+  if (NEED_J) {
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    if (threadIdx.x < 32) tmem::dealloc(tmem_base, kHexTmCols);
+  }
 }
 
 }  // namespace
