@@ -587,8 +587,10 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
           multi_fixup_one(pv.multi, i, L, pv.partials, R, vals);
         named_sync(kBarScat, kWsHalf);
         if (tb == 0) {
-          __threadfence();
-          asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(pv.flags + pv.n_patches + 2), "r"(1) : "memory");
+          // system scope: the flag releases the ghost rows to the side stream's
+          // copy engine / NCCL kernels, not only to this GPU's SMs
+          __threadfence_system();
+          asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(pv.flags + pv.n_patches + 2), "r"(1) : "memory");
         }
       }
     }
