@@ -50,7 +50,10 @@ struct HexIn {
 //   grad_xy N_(j,l) = f_l P_j + s_l Q_j K,  P_j = A^-T grad_(xi,eta) Q_j,
 //   K = -A^-T c / z_zeta,   d/dz N_(j,l) = s_l Q_j / z_zeta
 // (exactly the isoparametric gradient; no general 3 x 3 inverse)
-__device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8], double G[8][3]) {
+// pk (if not null): the point's column-structure data for the TMEM cache of
+// KH-patch: P_j (x, y) for j = 0..3, 1 / z_zeta, K (x, y)
+__device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8], double G[8][3],
+                                            double* pk = nullptr) {
   constexpr double gz = 0.57735026918962576451;
   const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
   const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
@@ -85,8 +88,44 @@ __device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8],
     G[j + 4][0] = fma(f1, px, hq * kx);
     G[j + 4][1] = fma(f1, py, hq * ky);
     G[j + 4][2] = hq * iz;
+    if (pk) { pk[2 * j] = px; pk[2 * j + 1] = py; }
   }
+  if (pk) { pk[8] = iz; pk[9] = kx; pk[10] = ky; }
   return detA * zz;   // Gauss weights 1
+}
+
+// KH-patch TMEM row of an element thread (doubles take 2 columns): per point
+// qp the 7-double record [e1x, exy, exz, e2y, eyz, c, d] and K (x, y) at
+// 18 qp; per footprint point m = qp & 3 (P_j and 1 / z_zeta depend on
+// (xi, eta) only) P_j (x, y), j = 0..3, and 1 / z_zeta at kHexTmGeo + 18 m
+constexpr uint32_t kHexTmGeo = 144;
+constexpr uint32_t kHexTmCols = 256;   // allocation per CTA (216 used; 2 CTAs per SM)
+
+// passes 2 and 3: the gradients of point qp rebuilt from the cache,
+//   grad N_(j,0) = f_0 (P_j, 0) - Q_j / 2 (K, 1 / z_zeta),
+//   grad N_(j,1) = f_1 (P_j, 0) + Q_j / 2 (K, 1 / z_zeta)
+// (hex_point's formula), and the point's record
+__device__ __forceinline__ void hex_grad_tm(uint32_t tm, int qp, double G[8][3], double rec[7]) {
+  constexpr double gz = 0.57735026918962576451;
+  const double xi = (qp & 1) ? gz : -gz, eta = (qp & 2) ? gz : -gz, zeta = (qp & 4) ? gz : -gz;
+  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+  const double f0 = 0.5 * (1.0 - zeta), f1 = 0.5 * (1.0 + zeta);
+  double rk[9], pz[9];
+  tmem::ld<9>(tm + 18 * qp, rk);
+  tmem::ld<9>(tm + kHexTmGeo + 18 * (qp & 3), pz);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double hq = 0.125 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+    const double hx = hq * rk[7], hy = hq * rk[8], hz = hq * pz[8];
+    G[j][0] = fma(f0, pz[2 * j], -hx);
+    G[j][1] = fma(f0, pz[2 * j + 1], -hy);
+    G[j][2] = -hz;
+    G[j + 4][0] = fma(f1, pz[2 * j], hx);
+    G[j + 4][1] = fma(f1, pz[2 * j + 1], hy);
+    G[j + 4][2] = hz;
+  }
+#pragma unroll
+  for (int i = 0; i < 7; ++i) rec[i] = rk[i];
 }
 
 // viscosity factors and the strain-rate gradients g_{a,i} = eps_a . grad phi_i
@@ -450,7 +489,6 @@ __host__ __device__ constexpr int dmap4(int p, int p2) {
              : 4 * ((p >> 1) * (7 - (p >> 1)) / 2 + ((p2 >> 1) - (p >> 1) - 1)) + 2 * (p & 1) + (p2 & 1);
 }
 constexpr int kHexDR = 36;   // residual entries of D: 36 + 2 j + a
-constexpr uint32_t kHexTmCols = 128;   // TMEM per CTA: 8 point records x 7 doubles per thread
 constexpr int kPlanOffsetQ = (kHexDE + kHexOE) * TPQ * 8 / 16 * 16 + 16;
 constexpr int kPlanOffsetQR = kHexDE * TPQ * 8 / 16 * 16 + 16;
 
@@ -607,12 +645,15 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int i = 0; i < 36; ++i) bb[i] = 0.0;
 #pragma unroll 1
         for (int qp = 0; qp < 8; ++qp) {
-          double N[8], G[8][3], g[16], c, d;
-          const double W = hex_point(h, qp, N, G);
+          double N[8], G[8][3], g[16], c, d, pk[11];
+          const double W = hex_point(h, qp, N, G, NEED_J ? pk : nullptr);
           if (NEED_J) {
-            double rec[7];
+            double rec[9];
             hex_visc_rec<N3>(h, G, W, kp, g, c, d, rec);
-            tmem::st<7>(tm + 14 * qp, rec);
+            rec[7] = pk[9];
+            rec[8] = pk[10];
+            tmem::st<9>(tm + 18 * qp, rec);
+            if (qp < 4) tmem::st<9>(tm + kHexTmGeo + 18 * qp, pk);
           } else {
             hex_visc<N3>(h, G, W, kp, g, c, d);
           }
@@ -625,7 +666,19 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
             r[2 * i] += fma(c, g[2 * i], bw * sx * N[i]);
             r[2 * i + 1] += fma(c, g[2 * i + 1], bw * sy * N[i]);
           }
-          if (NEED_J) hex_accum<0>(G, g, c, d, bb);
+        }
+        // (bottom, bottom) block in a pass of its own from the TMEM cache: pass 1
+        // then holds only the residual (no spills in its point loop; with the
+        // block accumulated in pass 1: 400 B of spills, 6.91 vs 5.83 ms)
+        if (NEED_J) {
+          tmem::wait_st();
+#pragma unroll 1
+          for (int qp = 0; qp < 8; ++qp) {
+            double G[8][3], g[16], c, d, rec[7];
+            hex_grad_tm(tm, qp, G, rec);
+            hex_g_rec(G, rec, g, c, d);
+            hex_accum<0>(G, g, c, d, bb);
+          }
         }
         if (k == 0) hex_basal<NEED_J>(h, r, bb);
         if (active) {
@@ -650,11 +703,8 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int i = 0; i < 64; ++i) bt[i] = 0.0;
 #pragma unroll 1
         for (int qp = 0; qp < 8; ++qp) {
-          double N[8], G[8][3], g[16], c, d;
-          const double W = hex_point(h, qp, N, G);
-          (void)W;
-          double rec[7];
-          tmem::ld<7>(tm + 14 * qp, rec);
+          double G[8][3], g[16], c, d, rec[7];
+          hex_grad_tm(tm, qp, G, rec);
           hex_g_rec(G, rec, g, c, d);
           hex_accum<1>(G, g, c, d, bt);
         }
@@ -668,11 +718,8 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int i = 0; i < 36; ++i) tt[i] = 0.0;
 #pragma unroll 1
         for (int qp = 0; qp < 8; ++qp) {
-          double N[8], G[8][3], g[16], c, d;
-          const double W = hex_point(h, qp, N, G);
-          (void)W;
-          double rec[7];
-          tmem::ld<7>(tm + 14 * qp, rec);
+          double G[8][3], g[16], c, d, rec[7];
+          hex_grad_tm(tm, qp, G, rec);
           hex_g_rec(G, rec, g, c, d);
           hex_accum<2>(G, g, c, d, tt);
         }
@@ -685,9 +732,11 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
     }
     if (k == 0) bulk_wait(&plan_bar);
     __syncthreads();
+#ifndef FO_PROBE_HEX_NO_B   // timing probe only: the element alone (wrong values)
     if (NEED_J) {
       if (k < L) phase_bq_j<true>(sp, k, L, D, O, vals, pv.partials, threadIdx.x, blockDim.x);
     }
+#endif
     phase_bq_r(sp, k, L, D + kHexDR * TPQ, R, pv.partials, threadIdx.x, blockDim.x);
     __syncthreads();
     if (active) {   // the held top block becomes level k+1's diagonal block
