@@ -569,18 +569,34 @@ __device__ __forceinline__ void phase_bq_r(const SmemPlan& sp, int kk, int L, co
   }
 }
 
+// threads per CTA: one per quad of a patch (kPatchQuads = 3 warps) plus a
+// fourth warp (the register file holds 2 CTAs x 128 x 255 registers) that
+// zero-fills the patch's lead boundary columns in-kernel while the element
+// warps compute layer 0 and then joins phase B (700 x 700 x 10 R + J 5.86 ->
+// 5.61 ms; FO_HEX_BLOCK=96: three warps and the zero kernel)
+#ifndef FO_HEX_BLOCK
+#define FO_HEX_BLOCK 128
+#endif
+constexpr int kHexBlock = FO_HEX_BLOCK;
+static_assert(kHexBlock >= kPatchQuads && kHexBlock % 32 == 0, "hex block");
+
 template <bool NEED_J, bool N3>
-__global__ void __launch_bounds__(kPatchQuads, kHexCtasPerSm)
+__global__ void __launch_bounds__(kHexBlock, kHexCtasPerSm)
 kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads,
                 const double* __restrict__ sigma, const double* __restrict__ Aw, KParams kp, PlanView pv,
                 const double* __restrict__ U, double* __restrict__ R, double* __restrict__ vals) {
   extern __shared__ __align__(16) double smem[];
   double* const D = smem;                  // [kHexDE][TPQ]
   double* const O = smem + kHexDE * TPQ;   // [kHexOE][TPQ] (R + J)
-  const int p = int(blockIdx.x);
-  const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   __shared__ uint64_t plan_bar;
   __shared__ uint32_t tmem_base;
+  __shared__ int ticket;
+  // in-kernel zero fill (pv.inkz, kHexBlock > kPatchQuads): patches in ticket
+  // order, so a lead patch (lower ticket) is already running when waited for
+  if (pv.inkz && threadIdx.x == 0) ticket = atomicAdd(pv.flags + pv.n_patches, 1);
+  if (pv.inkz) __syncthreads();
+  const int p = pv.inkz ? ticket : int(blockIdx.x);
+  const int t0 = __ldg(pv.t_begin + p), nt = __ldg(pv.t_begin + p + 1) - t0;
   SmemPlan sp;
   {
     const int c0 = __ldg(pv.col_ptr + p), c1 = __ldg(pv.col_ptr + p + 1);
@@ -604,10 +620,10 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
   const bool active = tl < nt;
   // tcgen05.ld / st are warp-collective: lanes without a quad evaluate a copy
   // of the patch's last one and publish nothing
-  const bool run = NEED_J ? true : active;
+  const bool run = tl < kPatchQuads && (NEED_J ? true : active);
   const int qi = t0 + (active ? tl : nt - 1);
   const uint32_t tm = tmem_base + (uint32_t(tl & ~31) << 16);   // this warp's lane quarter
-  const QuadRec qr = quads[qi];
+  const QuadRec qr = quads[run ? qi : t0];
   if (active) {
 #pragma unroll
     for (int i = 0; i < kHexDE; ++i) D[i * TPQ + tl] = 0.0;
@@ -616,6 +632,41 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
   for (int i = threadIdx.x; i < kHexDE; i += blockDim.x) D[i * TPQ + kPatchQuads] = 0.0;
   if (NEED_J)
     for (int i = threadIdx.x; i < kHexOE; i += blockDim.x) O[i * TPQ + kPatchQuads] = 0.0;
+  if (kHexBlock > kPatchQuads && pv.inkz && threadIdx.x >= kPatchQuads && threadIdx.x < kPatchQuads + 32) {
+    // the phase-B warp, while the element warps compute layer 0: zero-fill the
+    // boundary columns this patch leads, raise its flag, then wait for the
+    // leads of its other boundary columns (the first RED follows the CTA
+    // barrier before phase B of level 0)
+    const int lane = threadIdx.x & 31;
+    const int z0 = __ldg(pv.zl_ptr + p), z1 = __ldg(pv.zl_ptr + p + 1);
+    for (int i = z0; i < z1; ++i) {
+      const int c = __ldg(pv.zl + i);
+      for (int j = lane; j < L + 1; j += 32)
+        *reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)) = make_double2(0.0, 0.0);
+      if (NEED_J) {
+        const long long csn = __double_as_longlong(__ldg(reinterpret_cast<const double*>(col + c) + 5));
+        double2* v = reinterpret_cast<double2*>(vals + (csn >> 8));
+        const int64_t len2 = int64_t(2 * (csn & 255)) * (3 * L + 1);
+        for (int64_t j = lane; j < len2; j += 32) v[j] = make_double2(0.0, 0.0);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();   // the warp's zero stores (ordered by __syncwarp) before the flag
+      asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(pv.flags + p), "r"(1) : "memory");
+    }
+    const int w0 = __ldg(pv.wl_ptr + p), w1 = __ldg(pv.wl_ptr + p + 1);
+    for (int i = w0 + lane; i < w1; i += 32) {
+      const int32_t* f = pv.flags + __ldg(pv.wl + i);
+      int v = 0;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) break;
+        __nanosleep(64);
+      }
+    }
+    __syncwarp();
+  }
   double held[kHexDE];
   for (int k = 0; k < L; ++k) {
     if (run) {
@@ -965,13 +1016,15 @@ fo_status hex_create_impl(const fo_params* p, int64_t n_vert, const double* xy, 
 // KH-patch: zero fill of boundary columns, the patch kernel, the multi fix-up
 static fo_status launch_hex_owner(fo_mesh m, const double* d_U, double* R, double* d_vals, cudaStream_t s) {
   int launches = 0;
-  fo_status st = launch_owner_prologue(m, R, d_vals, s, &launches);
+  // a phase-B warp beside the element warps zero-fills in-kernel (no zero kernel)
+  constexpr bool inkz = kHexBlock > kPatchQuads;
+  fo_status st = launch_owner_prologue(m, R, d_vals, s, &launches, inkz);
   if (st) return st;
   const bool n3 = m->p.glen_n == 3.0;
   const KParams kp = make_kparams(m);
   PlanView pv{m->d_plan.t_begin, m->d_plan.col_ptr, m->d_plan.pair_ptr, m->d_plan.nedge, m->d_plan.blob,
               m->d_plan.blob_off, m->d_plan.partials, 0, m->d_plan.zl, m->d_plan.zl_ptr, m->d_plan.wl,
-              m->d_plan.wl_ptr, m->d_plan.flags, 0, m->plan.n_patches, m->d_plan.multi, 0, 0, 0};
+              m->d_plan.wl_ptr, m->d_plan.flags, inkz ? 1 : 0, m->plan.n_patches, m->d_plan.multi, 0, 0, 0};
   const size_t sm = size_t(d_vals ? kPlanOffsetQ : kPlanOffsetQR) + kPlanBytesHex;
   auto go = [&](auto kern) -> fo_status {
     fo_status e = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
@@ -983,7 +1036,7 @@ static fo_status launch_hex_owner(fo_mesh m, const double* d_U, double* R, doubl
       cudaEventCreate(&e1);
       cudaEventRecord(e0, s);
     }
-    kern<<<m->plan.n_patches, kPatchQuads, sm, s>>>(m->d_col, m->d_quad, m->d_sigma, m->d_A, kp, pv, d_U, R, d_vals);
+    kern<<<m->plan.n_patches, kHexBlock, sm, s>>>(m->d_col, m->d_quad, m->d_sigma, m->d_A, kp, pv, d_U, R, d_vals);
     if (m->timing) {
       cudaEventRecord(e1, s);
       m->timed.push_back({e0, e1});

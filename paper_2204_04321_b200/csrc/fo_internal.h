@@ -270,7 +270,8 @@ fo_status launch_jacobian(fo_mesh m, const double* d_U, double* d_R, double* d_v
                           void* stream);
 fo_status build_patch_plan(fo_mesh m, bool upload = true);
 // owner-computes assembly pieces (fo_owner.cu)
-fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
+fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches,
+                                bool inkz = false);
 fo_status launch_owner_fixup(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches);
 fo_status launch_owner_overlap(fo_mesh m, const double* d_U, double* d_R, double* d_vals, cudaStream_t s,
                                cudaStream_t side, cudaEvent_t ev0,

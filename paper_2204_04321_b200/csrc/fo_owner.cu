@@ -784,14 +784,15 @@ fo_status owner_multi(OwnerCall& c, cudaStream_t s, int r0, int r1) {
 }  // namespace
 
 // the owner-computes prologue / epilogue for the hexahedral patch kernel
-// (fo_hex.cu): class-C residual zero + boundary-column zero fill, and the
-// multi-column fix-up; `launches` counts the kernels enqueued
-fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches) {
+// (fo_hex.cu): class-C residual zero + boundary-column zero fill (inkz: the
+// kernel's flags and ticket reset instead), and the multi-column fix-up;
+// `launches` counts the kernels enqueued
+fo_status launch_owner_prologue(fo_mesh m, double* R, double* vals, cudaStream_t s, int* launches, bool inkz) {
   OwnerCall c;
   c.m = m;
   c.R = R;
   c.vals = vals;
-  fo_status st = owner_prologue(c, s);
+  fo_status st = owner_prologue(c, s, inkz);
   *launches += c.launches;
   return st;
 }
