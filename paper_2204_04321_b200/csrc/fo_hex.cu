@@ -95,11 +95,14 @@ __device__ __forceinline__ double hex_point(const HexIn& h, int qp, double N[8],
 }
 
 // KH-patch TMEM row of an element thread (doubles take 2 columns): per point
-// qp the 7-double record [e1x, exy, exz, e2y, eyz, c, d] and K (x, y) at
-// 18 qp; per footprint point m = qp & 3 (P_j and 1 / z_zeta depend on
-// (xi, eta) only) P_j (x, y), j = 0..3, and 1 / z_zeta at kHexTmGeo + 18 m
-constexpr uint32_t kHexTmGeo = 144;
-constexpr uint32_t kHexTmCols = 256;   // allocation per CTA (216 used; 2 CTAs per SM)
+// qp the 7-double record [e1x, exy, exz, e2y, eyz, c, d], K (x, y) and
+// c / (2 z_zeta^2) at 20 qp; per footprint point m = qp & 3 (P_j and
+// 1 / z_zeta depend on (xi, eta) only) P_j (x, y), j = 0..3, and 1 / z_zeta at
+// kHexTmGeo + 18 m; the vertical-derivative sums T (hex_zz) at kHexTmT
+constexpr uint32_t kHexTmRec = 20;
+constexpr uint32_t kHexTmGeo = 160;
+constexpr uint32_t kHexTmT = 232;
+constexpr uint32_t kHexTmCols = 256;   // allocation per CTA (252 used; 2 CTAs per SM)
 
 // passes 2 and 3: the gradients of point qp rebuilt from the cache,
 //   grad N_(j,0) = f_0 (P_j, 0) - Q_j / 2 (K, 1 / z_zeta),
@@ -111,7 +114,7 @@ __device__ __forceinline__ void hex_grad_tm(uint32_t tm, int qp, double G[8][3],
   const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
   const double f0 = 0.5 * (1.0 - zeta), f1 = 0.5 * (1.0 + zeta);
   double rk[9], pz[9];
-  tmem::ld<9>(tm + 18 * qp, rk);
+  tmem::ld<9>(tm + kHexTmRec * qp, rk);
   tmem::ld<9>(tm + kHexTmGeo + 18 * (qp & 3), pz);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -436,28 +439,90 @@ hex_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quads, co
 // uv: c Gx Gy' + (c Gy / 2) Gx', vu: (c Gx / 2) Gy' + c Gy Gx', H of SURVEY.md
 // App. A.3): 3-4 FMA per entry instead of hex_jentry's products per entry.
 // BLK 0: (bottom, bottom) packed p <= p2 (36); 1: (bottom, top) [8 p + p2] (64);
-// 2: (top, top) packed (36).
+// 2: (top, top) packed (36).  The (c / 2) G_z G_z' part of the uu and vv
+// entries is left out here and added once per block by hex_zz.
+//
+// hex_zz: G_z of node (j, l) is -/+ Q_j / (2 z_zeta) (l = 0 / 1) and Q_j, z_zeta
+// depend on the footprint point m only, so over the 8 points
+//   sum_q (c_q / 2) G_z(j,l) G_z(j2,l2) = s(l) s(l2) T(j, j2),
+//   T(j, j2) = sum_m (Q_j Q_j2 / 4)(m) sum_zeta c / (2 z_zeta^2),
+// s(0) = -1, s(1) = +1: 10 numbers per hexahedron instead of two FMA per
+// entry and point.  T is built after pass 1 and added with sign +
+// ((bottom, bottom), (top, top)) or - ((bottom, top)).
+__device__ __forceinline__ void hex_zz_build(uint32_t tm) {
+  constexpr double gz = 0.57735026918962576451;
+  const double cxi[4] = {-1.0, 1.0, 1.0, -1.0}, ceta[4] = {-1.0, -1.0, 1.0, 1.0};
+  double w[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double a, b;
+    tmem::ld1(tm + kHexTmRec * m + 18, &a);
+    tmem::ld1(tm + kHexTmRec * (m + 4) + 18, &b);
+    w[m] = a + b;
+  }
+  double T[10];
+  int e = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int j2 = j; j2 < 4; ++j2) {
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double xi = (m & 1) ? gz : -gz, eta = (m & 2) ? gz : -gz;
+        const double hq = 0.125 * (1.0 + cxi[j] * xi) * (1.0 + ceta[j] * eta);
+        const double hq2 = 0.125 * (1.0 + cxi[j2] * xi) * (1.0 + ceta[j2] * eta);
+        t = fma(hq * hq2, w[m], t);   // (Q_j / 2)(Q_j2 / 2): compile-time constants
+      }
+      T[e++] = t;
+    }
+  tmem::st<10>(tm + kHexTmT, T);
+}
+__host__ __device__ constexpr int tidx4(int j, int j2) {
+  return j <= j2 ? j * 4 - (j * (j - 1)) / 2 + (j2 - j) : j2 * 4 - (j2 * (j2 - 1)) / 2 + (j - j2);
+}
+// add +/- T to the uu / vv entries of a block in hex_accum's layout
+template <int BLK>
+__device__ __forceinline__ void hex_zz_add(uint32_t tm, double* acc) {
+  double T[10];
+  tmem::ld<10>(tm + kHexTmT, T);
+  auto sym = [](int a, int b) { return a * 8 - (a * (a - 1)) / 2 + (b - a); };
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2) {
+      if (BLK != 1 && j2 < j) continue;
+      const double t = T[tidx4(j, j2)];
+      if (BLK == 1) {
+        acc[8 * (2 * j) + 2 * j2] -= t;
+        acc[8 * (2 * j + 1) + 2 * j2 + 1] -= t;
+      } else {
+        acc[sym(2 * j, 2 * j2)] += t;
+        acc[sym(2 * j + 1, 2 * j2 + 1)] += t;
+      }
+    }
+}
 template <int BLK>
 __device__ __forceinline__ void hex_accum(const double G[8][3], const double g[16], double c, double d,
                                           double* acc) {
   constexpr int r0 = BLK == 2 ? 4 : 0, c0 = BLK == 0 ? 0 : 4;
 #pragma unroll
   for (int i = r0; i < r0 + 4; ++i) {
-    const double cx = c * G[i][0], cy = c * G[i][1], cz = c * G[i][2];
-    const double ax = 2.0 * cx, ay = 0.5 * cy, az = 0.5 * cz, bx = 0.5 * cx, by = 2.0 * cy;
+    const double cx = c * G[i][0], cy = c * G[i][1];
+    const double ax = 2.0 * cx, ay = 0.5 * cy, bx = 0.5 * cx, by = 2.0 * cy;
     const double du = -d * g[2 * i], dv = -d * g[2 * i + 1];
 #pragma unroll
     for (int i2 = c0; i2 < c0 + 4; ++i2) {
       if (BLK != 1 && i2 < i) continue;
-      const double gx = G[i2][0], gy = G[i2][1], gz = G[i2][2];
+      const double gx = G[i2][0], gy = G[i2][1];
       const int p = 2 * (i - r0), p2 = 2 * (i2 - c0);
       auto sym = [](int a, int b) { return a * 8 - (a * (a - 1)) / 2 + (b - a); };
       double& euu = BLK == 1 ? acc[8 * p + p2] : acc[sym(p, p2)];
       double& euv = BLK == 1 ? acc[8 * p + p2 + 1] : acc[sym(p, p2 + 1)];
       double& evv = BLK == 1 ? acc[8 * (p + 1) + p2 + 1] : acc[sym(p + 1, p2 + 1)];
-      euu = fma(du, g[2 * i2], fma(az, gz, fma(ay, gy, fma(ax, gx, euu))));
+      euu = fma(du, g[2 * i2], fma(ay, gy, fma(ax, gx, euu)));
       euv = fma(du, g[2 * i2 + 1], fma(ay, gx, fma(cx, gy, euv)));
-      evv = fma(dv, g[2 * i2 + 1], fma(az, gz, fma(by, gy, fma(bx, gx, evv))));
+      evv = fma(dv, g[2 * i2 + 1], fma(by, gy, fma(bx, gx, evv)));
       if (BLK == 1 || i2 != i) {
         double& evu = BLK == 1 ? acc[8 * (p + 1) + p2] : acc[sym(p + 1, p2)];
         evu = fma(dv, g[2 * i2], fma(cy, gx, fma(bx, gy, evu)));
@@ -699,11 +764,12 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
           double N[8], G[8][3], g[16], c, d, pk[11];
           const double W = hex_point(h, qp, N, G, NEED_J ? pk : nullptr);
           if (NEED_J) {
-            double rec[9];
+            double rec[10];
             hex_visc_rec<N3>(h, G, W, kp, g, c, d, rec);
             rec[7] = pk[9];
             rec[8] = pk[10];
-            tmem::st<9>(tm + 18 * qp, rec);
+            rec[9] = 0.5 * c * pk[8] * pk[8];   // hex_zz
+            tmem::st<10>(tm + kHexTmRec * qp, rec);
             if (qp < 4) tmem::st<9>(tm + kHexTmGeo + 18 * qp, pk);
           } else {
             hex_visc<N3>(h, G, W, kp, g, c, d);
@@ -723,6 +789,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         // block accumulated in pass 1: 400 B of spills, 6.91 vs 5.83 ms)
         if (NEED_J) {
           tmem::wait_st();
+          hex_zz_build(tm);
 #pragma unroll 1
           for (int qp = 0; qp < 8; ++qp) {
             double G[8][3], g[16], c, d, rec[7];
@@ -730,6 +797,8 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
             hex_g_rec(G, rec, g, c, d);
             hex_accum<0>(G, g, c, d, bb);
           }
+          tmem::wait_st();
+          hex_zz_add<0>(tm, bb);
         }
         if (k == 0) hex_basal<NEED_J>(h, r, bb);
         if (active) {
@@ -759,6 +828,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
           hex_g_rec(G, rec, g, c, d);
           hex_accum<1>(G, g, c, d, bt);
         }
+        hex_zz_add<1>(tm, bt);
         if (active) {
 #pragma unroll
           for (int i = 0; i < 64; ++i) O[i * TPQ + tl] = bt[i];
@@ -774,6 +844,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
           hex_g_rec(G, rec, g, c, d);
           hex_accum<2>(G, g, c, d, tt);
         }
+        hex_zz_add<2>(tm, tt);
         int e = 0;
 #pragma unroll
         for (int pp = 0; pp < 8; ++pp)
