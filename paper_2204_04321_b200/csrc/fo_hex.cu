@@ -643,6 +643,19 @@ __device__ __forceinline__ void phase_bq_r(const SmemPlan& sp, int kk, int L, co
 #define FO_HEX_BLOCK 128
 #endif
 constexpr int kHexBlock = FO_HEX_BLOCK;
+// unroll factors of the point loops (pass 1, the (bottom,bottom) / (top,top)
+// passes, the (bottom,top) pass): 1 / 2 / 2 -- 5.38 -> 5.31 ms; pass 1 x2
+// spills (5.50 ms), profiles/r02ah_ab_hex_unroll.txt
+#ifndef FO_HEX_U_P1
+#define FO_HEX_U_P1 1
+#endif
+#ifndef FO_HEX_U_BB
+#define FO_HEX_U_BB 2
+#endif
+#ifndef FO_HEX_U_BT
+#define FO_HEX_U_BT 2
+#endif
+constexpr int kHexUP1 = FO_HEX_U_P1, kHexUBB = FO_HEX_U_BB, kHexUBT = FO_HEX_U_BT;
 static_assert(kHexBlock >= kPatchQuads && kHexBlock % 32 == 0, "hex block");
 
 template <bool NEED_J, bool N3>
@@ -759,7 +772,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         for (int i = 0; i < 16; ++i) r[i] = 0.0;
 #pragma unroll
         for (int i = 0; i < 36; ++i) bb[i] = 0.0;
-#pragma unroll 1
+#pragma unroll kHexUP1
         for (int qp = 0; qp < 8; ++qp) {
           double N[8], G[8][3], g[16], c, d, pk[11];
           const double W = hex_point(h, qp, N, G, NEED_J ? pk : nullptr);
@@ -790,7 +803,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         if (NEED_J) {
           tmem::wait_st();
           hex_zz_build(tm);
-#pragma unroll 1
+#pragma unroll kHexUBB
           for (int qp = 0; qp < 8; ++qp) {
             double G[8][3], g[16], c, d, rec[7];
             hex_grad_tm(tm, qp, G, rec);
@@ -821,7 +834,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         double bt[64];
 #pragma unroll
         for (int i = 0; i < 64; ++i) bt[i] = 0.0;
-#pragma unroll 1
+#pragma unroll kHexUBT
         for (int qp = 0; qp < 8; ++qp) {
           double G[8][3], g[16], c, d, rec[7];
           hex_grad_tm(tm, qp, G, rec);
@@ -837,7 +850,7 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
         double tt[36];
 #pragma unroll
         for (int i = 0; i < 36; ++i) tt[i] = 0.0;
-#pragma unroll 1
+#pragma unroll kHexUBB
         for (int qp = 0; qp < 8; ++qp) {
           double G[8][3], g[16], c, d, rec[7];
           hex_grad_tm(tm, qp, G, rec);
