@@ -70,6 +70,8 @@ def parse_args():
                     help="N > 1: fo_assemble_jacobian_halo (export overlapped with the interior patches, "
                          "default) or fo_assemble_jacobian then fo_halo_sum")
     ap.add_argument("--no-eta", action="store_true", help="N > 1: skip the one-GPU base run of the efficiency")
+    ap.add_argument("--no-next-rows", action="store_true",
+                    help="N = 1: skip the SURVEY.md 8(f) f4 lines (tetrahedra on C3, hexahedra 700 x 700 x 10)")
     return ap.parse_args()
 
 
@@ -708,6 +710,46 @@ def main():
                    "formula": "((t1/N1)/(tn/Nn))/n, N = wedges (PAPER.md P:531-535)"}
         dist.barrier()
 
+    # SURVEY.md 8(f) f4 at N = 1 (not part of the step): R + J with three P1
+    # tetrahedra per prism on the same C3 mesh, and 8-node hexahedra on a
+    # 700 x 700 quad footprint x 10 layers (4.9 M elements, 548 M nonzeros);
+    # device time per assembly with the step's protocol (median, L2 flushed)
+    next_rows = None
+    if world == 1 and not args.no_next_rows:
+        def med_ms(fn, n=7):
+            for _ in range(3):
+                fn()
+            out = []
+            for _ in range(n):
+                flush.fill_(0.5)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                b.synchronize()
+                out.append(a.elapsed_time(b))
+            return statistics.median(out)
+        from paper_2204_04321_b200 import meshgen as mg
+        mesh.set_element(1)
+        t_ms = med_ms(lambda: mesh.jacobian(U, graph, R, V))
+        mesh.set_element(0)
+        fq = mg.to_quads(mg.ismip_hom_a(nx=700, n_layers=10), 700)
+        mq = fo.Mesh.from_footprint(fq, device=dev.index)
+        gq = mq.graph()
+        Uq = torch.tensor(fq.U, device=dev)
+        Rq = torch.empty(mq.n_dofs, dtype=torch.float64, device=dev)
+        Vq = torch.empty(gq.nnz, dtype=torch.float64, device=dev)
+        h_ms = med_ms(lambda: mq.jacobian(Uq, gq, Rq, Vq))
+        next_rows = {
+            "f4_tet3": {"elements": 3 * mesh.n_elems, "ms": t_ms, "value": 3 * mesh.n_elems / t_ms / 1e3,
+                        "unit": "Melem/s", "workload": "C3, three P1 tetrahedra per prism (reading L22)"},
+            "f4_hex8": {"elements": mq.n_elems, "nnz": gq.nnz, "ms": h_ms, "value": mq.n_elems / h_ms / 1e3,
+                        "unit": "Melem/s", "workload": "700 x 700 quads x 10 layers, 8-node trilinear hexahedra "
+                                                       "(reading L23)"},
+            "note": "R + J device time per assembly, median of 7 after 3 warm-ups, 512 MB written before each"}
+        del mq, gq, Uq, Rq, Vq
+
     loop = None
     if world == 1 and args.loopback > 1:
         loop = loopback_run(fp, args.loopback, args.steps, args.warmup, dev, flush, stream)
@@ -740,7 +782,8 @@ def main():
                        "scatter": {0: "owner-computes", 1: "atomic", 2: "owner-computes (ws)", 3: "owner-computes (round-1 kernel)"}[args.scatter],
                        "l2": "1.7 GB of CSR values written per step (> 126 MB L2) and a 512 MB buffer "
                              "written between timed steps"},
-            "roofline": roof, "residual_only": residual_only, "graph_100": graph100, "e2e": e2e,
+            "roofline": roof, "residual_only": residual_only, "graph_100": graph100, "next_rows": next_rows,
+            "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk, "cpu_baseline": cpu,
             "per_step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
