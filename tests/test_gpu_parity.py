@@ -577,3 +577,35 @@ def test_c3_repeated_assemblies_bitwise_on_device(torch_cuda):
         bad += int(not torch.equal(V, V0)) + int(not torch.equal(R, R0))
     torch.cuda.synchronize()
     assert bad == 0
+
+
+def test_hexahedra_repeated_assemblies_bitwise_on_device(torch_cuda):
+    """Stress of the quad-patch kernel's in-kernel zero fill (the fourth warp
+    of each CTA: atomic patch tickets, lead flags, waits) and of its boundary
+    REDs: 30 back-to-back R + J assemblies of 250 x 250 quads x 6 layers (~650
+    patches, several waves of two CTAs per SM) into NaN-poisoned buffers, each
+    equal bit for bit to the first, which is NaN-free; the residual-only path
+    (zero kernel) likewise."""
+    import torch
+    from paper_2204_04321_b200 import fo
+    fp = mg.to_quads(mg.ismip_hom_a(nx=250, n_layers=6), 250)
+    mesh = fo.Mesh.from_footprint(fp)
+    g = mesh.graph()
+    U = torch.tensor(fp.U, device="cuda")
+    R = torch.full((mesh.n_dofs,), float("nan"), dtype=torch.float64, device="cuda")
+    V = torch.full((g.nnz,), float("nan"), dtype=torch.float64, device="cuda")
+    mesh.jacobian(U, g, R, V)
+    R0, V0 = R.clone(), V.clone()
+    assert not torch.isnan(V0).any() and not torch.isnan(R0).any()
+    Rr = torch.full((mesh.n_dofs,), float("nan"), dtype=torch.float64, device="cuda")
+    mesh.residual(U, Rr)
+    assert not torch.isnan(Rr).any()
+    assert torch.allclose(Rr, R0, rtol=0.0, atol=1e-12 * float(R0.abs().max()))
+    bad = 0
+    for _ in range(30):
+        R.fill_(float("nan"))
+        V.fill_(float("nan"))
+        mesh.jacobian(U, g, R, V)
+        bad += int(not torch.equal(V, V0)) + int(not torch.equal(R, R0))
+    torch.cuda.synchronize()
+    assert bad == 0
