@@ -541,12 +541,11 @@ ka_ws_kernel(const ColRec* __restrict__ col, const TriRec* __restrict__ tris,
       const int lane = tb & 31;
       for (int i = z0 + (tb >> 5); i < z1; i += kWsHalf / 32) {
         const int c = __ldg(pv.zl + i);
-        for (int j = lane; j < L + 1; j += 32)
-          *reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)) = make_double2(0.0, 0.0);
+        for (int j = lane; j < L + 1; j += 32) zero2(reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)));
         const long long csn = __double_as_longlong(__ldg(reinterpret_cast<const double*>(col + c) + 5));
         double2* v = reinterpret_cast<double2*>(vals + (csn >> 8));
         const int64_t len2 = int64_t(2 * (csn & 255)) * (3 * L + 1);
-        for (int64_t j = lane; j < len2; j += 32) v[j] = make_double2(0.0, 0.0);
+        for (int64_t j = lane; j < len2; j += 32) zero2(v + j);
       }
       named_sync(kBarScat, kWsHalf);
       if (tb == 0) {
