@@ -1,3 +1,4 @@
+# round-1 first GPU session (microbench, GPU tests, first C3 timing); kept for the record (dev tool)
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -m paper_2204_04321_b200._build --force
