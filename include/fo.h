@@ -125,10 +125,14 @@ FO_API fo_status fo_mesh_set_temperature(fo_mesh m, const double* T_star, double
  * every other argument as fo_mesh_create (A_elem[n_quad*L]).  Each layer
  * element is an 8-node trilinear hexahedron (reading L23: 2x2x2 Gauss,
  * isoparametric, exact Jacobian; basal term with 2x2 Gauss on the bilinear
- * bottom face).  Graph, SpMV, line preconditioner, A(T) apply unchanged; the
- * scatter is coloured (quads sharing a corner never run concurrently; a fixed
- * launch order makes it deterministic).  Single-domain; no lateral term, no
- * fo_set_element / atomic scatter.  Synchronous. */
+ * bottom face).  Graph, SpMV, line preconditioner, A(T) apply unchanged.  The
+ * default R + J scatter is the owner-computes quad-patch kernel (KH-patch:
+ * Hilbert-ordered patches of <= 96 quads, boundary columns zero-filled
+ * in-kernel and RED, multi columns by a fix-up; bitwise reproducible);
+ * FO_SCATTER_ATOMIC selects the coloured read-modify-write ablation (quads
+ * sharing a corner never run concurrently; a fixed launch order makes it
+ * deterministic), which also computes the residual alone.  Single-domain;
+ * no lateral term, no fo_set_element.  Synchronous. */
 FO_API fo_status fo_mesh_create_quad(const fo_params* p, int64_t n_vert, const double* xy,
                                      int64_t n_quad, const int32_t* quad, int32_t n_layers,
                                      const double* sigma, const double* thickness,

@@ -10,13 +10,16 @@
 // top, top-top) that re-evaluate the point data.
 // Basal term: 2 x 2 Gauss on the bilinear bottom face, true 3D area element.
 //
-// Scatter: COLOURED.  Quads are greedily coloured so that no two quads of a
-// colour share a corner; colour c, layer parity l launches touch disjoint node
-// sets, so each thread adds its block into the (zeroed) CSR values and residual
-// with plain read-modify-write, in a fixed launch order: deterministic.  CSR
-// positions come from the column structure (QuadRec slots), col_idx is not read.
-// The graph, SpMV and line preconditioner of the wedge path apply unchanged
-// (they only see columns and coupling lists).  Single-domain meshes.
+// R + J (default): KH-patch, the wedge path's owner-computes patch scheme on
+// quad patches (kh_patch_kernel below).
+// The residual alone and the FO_SCATTER_ATOMIC ablation: COLOURED.  Quads are
+// greedily coloured so that no two quads of a colour share a corner; colour c,
+// layer parity l launches touch disjoint node sets, so each thread adds its
+// block into the (zeroed) CSR values and residual with plain read-modify-write,
+// in a fixed launch order: deterministic.  CSR positions come from the column
+// structure (QuadRec slots), col_idx is not read.  The graph, SpMV and line
+// preconditioner of the wedge path apply unchanged (they only see columns and
+// coupling lists).  Single-domain meshes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
