@@ -379,10 +379,14 @@ constexpr int kWsThreads = 2 * kWsHalf;
 constexpr int kWsCtas = kWsHalf == 128 ? 2 : 1;
 constexpr uint32_t kWsAlloc = kTmCols * (kWsHalf / 128);   // TMEM columns per CTA
 #ifndef FO_WS_REGS_E
-#define FO_WS_REGS_E 200
+#define FO_WS_REGS_E 192
 #endif
-// setmaxnreg split: E + B = 2 x 128.  200 / 56: no spills in either warpgroup
-// (208 / 48 spilled the scatter's addresses: C3 1.471 vs 1.403 ms; 192 / 64: 1.496)
+// setmaxnreg split: E + B = 2 x 128.  192 / 64 (session 3 of round 2): no
+// spills in either warpgroup of either instance -- wedges 1.293 -> 1.280 ms
+// against 200 / 56 (which left the tetrahedral instance's scatter spilling:
+// C3-tet 1.418 -> 1.244 ms), profiles/r02ai_ab_regs.txt, r02ai_ab_tet.txt.
+// Earlier kernels: 200 / 56 vs 208 / 48 1.403 vs 1.471 ms (scatter spills),
+// 192 / 64 then 1.496 ms (element spills)
 constexpr int kWsRegsE = FO_WS_REGS_E, kWsRegsB = 256 - FO_WS_REGS_E;
 constexpr int kPlanOffsetWS = ((kD + kO) * TP * 8 + 15) / 16 * 16;
 constexpr int kUbufOffsetWS = (kPlanOffsetWS + kPlanBytes + 15) / 16 * 16;   // [3 levels x 3 nodes][TP] double2
