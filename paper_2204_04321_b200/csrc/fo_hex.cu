@@ -722,12 +722,13 @@ kh_patch_kernel(const ColRec* __restrict__ col, const QuadRec* __restrict__ quad
     const int z0 = __ldg(pv.zl_ptr + p), z1 = __ldg(pv.zl_ptr + p + 1);
     for (int i = z0; i < z1; ++i) {
       const int c = __ldg(pv.zl + i);
-      for (int j = lane; j < L + 1; j += 32) zero2(reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)));
+      for (int j = lane; j < L + 1; j += 32)
+        *reinterpret_cast<double2*>(R + 2 * (int64_t(c) * (L + 1) + j)) = make_double2(0.0, 0.0);
       if (NEED_J) {
         const long long csn = __double_as_longlong(__ldg(reinterpret_cast<const double*>(col + c) + 5));
         double2* v = reinterpret_cast<double2*>(vals + (csn >> 8));
         const int64_t len2 = int64_t(2 * (csn & 255)) * (3 * L + 1);
-        for (int64_t j = lane; j < len2; j += 32) zero2(v + j);
+        for (int64_t j = lane; j < len2; j += 32) v[j] = make_double2(0.0, 0.0);   // no L2 hint (slower here)
       }
     }
     __syncwarp();

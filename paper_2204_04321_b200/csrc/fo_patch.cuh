@@ -60,13 +60,15 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar) {
                  : "=r"(done) : "r"(b) : "memory");
 }
 
-// L2 eviction-priority hints (FO_L2HINT bits): 1 (default) = the interior
-// stores stream (evict_first: never re-read by the kernel; C3 DRAM 3.07 ->
-// 2.77 GB per launch, 1.301 -> 1.294 ms), 2 = the boundary zero fill and REDs
-// stay (evict_last: the other patch's RED reads the line; 2.65 GB with both
-// bits but 1.308 ms, not kept); profiles/r02ah_variants_l2hint.txt
+// L2 eviction-priority hints (FO_L2HINT bits, default 1 | 8): 1 = the
+// interior stores stream (evict_first: never re-read by the kernel; C3 DRAM
+// 3.07 -> 2.77 GB per launch, 1.301 -> 1.294 ms), 8 = the wedge kernel's
+// in-kernel zero fill stays (evict_last: a later patch's RED reads the line;
+// 2.76 -> 2.62 GB, 1.276 -> 1.273 ms; not for the hexahedral kernel, 5.32 ->
+// 5.37 ms), 2 = the zero fill and the REDs evict_last (2.65 GB but 1.308 ms,
+// not kept); profiles/r02ah_variants_l2hint.txt, r02aj_variants_zl.txt
 #ifndef FO_L2HINT
-#define FO_L2HINT 1
+#define FO_L2HINT 9
 #endif
 __device__ __forceinline__ uint64_t l2_policy_first() {
   uint64_t p;
@@ -87,7 +89,7 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 }
 // the in-kernel zero fill's stores
 __device__ __forceinline__ void zero2(double2* p) {
-  if (FO_L2HINT & 2)
+  if (FO_L2HINT & (2 | 8))   // 8: the zero fill alone (experiment)
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %1}, %2;" ::"l"(p), "d"(0.0), "l"(l2_policy_last())
                  : "memory");
   else
