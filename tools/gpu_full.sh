@@ -1,5 +1,7 @@
 # full round check on one B200: build, gpu tests, smoke, one ncu --set full
-# capture of the top kernel (-> profiles/ncu_summary.json, read by bench.py),
+# capture of the top kernel (-> profiles/ncu_summary.json on the box, read by
+# bench.py; gpurun merges only gpurun_out/ back, so copy
+# gpurun_out/ncu_summary.json to profiles/ here and commit it),
 # the ncu launch list of the bench command, then the bench (ours + reference)
 set -x
 TAG=${1:-r01}
