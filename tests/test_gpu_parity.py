@@ -166,12 +166,13 @@ def test_parity_tetrahedra(torch_cuda, ora_mod, case):
 
 @pytest.mark.parametrize("scatter", [0, 1])
 @pytest.mark.parametrize("case", ["C1-quads", "slab-quads-distorted", "quads-temperature", "quads-40x40",
-                                  "quads-33x33-distorted"])
+                                  "quads-33x33-distorted", "quads-1-layer"])
 def test_parity_hexahedra(torch_cuda, ora_mod, case, scatter):
     """NEXT-f4: quadrilateral footprint, 8-node trilinear hexahedra (P:478,
     reading L23): the quad-patch owner-computes kernel (scatter 0; the 40 x 40
     and 33 x 33 footprints span 17 / 12 patches, so boundary, multi and pad
-    handling are exercised) and the coloured read-modify-write ablation (1)."""
+    handling are exercised; one layer: levels 0 and L only) and the coloured
+    read-modify-write ablation (1)."""
     if case == "C1-quads":
         fp = mg.to_quads(mg.ismip_hom_a(nx=10, n_layers=5), 10)
     elif case == "slab-quads-distorted":
@@ -180,6 +181,8 @@ def test_parity_hexahedra(torch_cuda, ora_mod, case, scatter):
         fp = mg.to_quads(mg.ismip_hom_a(nx=40, n_layers=3), 40)
     elif case == "quads-33x33-distorted":
         fp = mg.to_quads(mg.slab(nx=33, n_layers=2, distort=0.2), 33)
+    elif case == "quads-1-layer":   # L = 1: the basal and surface levels only, 7 patches
+        fp = mg.to_quads(mg.ismip_hom_a(nx=26, n_layers=1), 26)
     else:
         fp = mg.with_temperature(mg.to_quads(mg.ismip_hom_a(nx=6, n_layers=3), 6))
     g = gpu_assemble(torch_cuda, fp, scatter=scatter)
